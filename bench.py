@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the hot path on B200: C += A.B, F16 inputs, at M=N=K=8192.
+
+One step = one F32-accumulate GEMM and one F16-accumulate GEMM (both modes the
+paper evaluates, Sec. 4.1 P:924-949 and Sec. 4.2; BASELINE.json
+metric "GEMM TFLOP/s & % of B200 dense FP16 peak at M=N=K=8192 (F32/F16 acc)").
+FLOPs = 2MNK per GEMM (the "+C" adds are not counted).
+
+    python bench.py [--gpus N --steps K --warmup W]       # our kernels (default)
+    python bench.py --impl reference ...                   # the CPU oracle, bounded sample
+
+Multi-GPU (torchrun, one rank per GPU): batches of independent matmuls, one
+problem per GPU (BASELINE.json configs[4] "batched one-per-GPU"; weak scaling,
+no data-path collective); time = max over ranks of the device-timed region.
+Inputs are seeded (synth/), uploaded to HBM before the timed region; the
+per-step working set (A 128 MB + B 128 MB + C 256/128 MB) exceeds the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "GEMM TFLOP/s & % of B200 dense FP16 peak at M=N=K=8192 (F32/F16 acc)"
+NOMINAL_F16_DENSE_TFLOPS = 2250.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--size", type=int, default=8192, help="M = N = K")
+    ap.add_argument("--modes", default="f32,f16")
+    ap.add_argument("--config", default="auto", help="kernel configuration (name in CONFIGS)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written), else the
+    fallback stated in B200_PROFILING.md (1.59 PFLOP/s burst, 6.65 TB/s)."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return {"tflops": float(mp["bf16_tflops"]), "tflops_sustained": float(mp.get("bf16_tflops_sustained", 0)),
+                "hbm_gbs": float(mp["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json bf16_tflops burst; "
+                "fp16 dense rate = bf16 rate, nominal ratio 1:1)"}
+    except (OSError, KeyError, ValueError):
+        return {"tflops": 1590.0, "tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+                "source": "fallback (B200_PROFILING.md: 1.59 PFLOP/s, 6.65 TB/s)"}
+
+
+class ClockSampler:
+    """NVML SM clock + clocks-event reasons, sampled in a thread during the timed region."""
+    NAMES = {
+        "nvmlClocksEventReasonGpuIdle": "gpu_idle",
+        "nvmlClocksEventReasonApplicationsClocksSetting": "applications_clocks_setting",
+        "nvmlClocksEventReasonSwPowerCap": "sw_power_cap",
+        "nvmlClocksEventReasonHwSlowdown": "hw_slowdown",
+        "nvmlClocksEventReasonSyncBoost": "sync_boost",
+        "nvmlClocksEventReasonSwThermalSlowdown": "sw_thermal_slowdown",
+        "nvmlClocksEventReasonHwThermalSlowdown": "hw_thermal_slowdown",
+        "nvmlClocksEventReasonHwPowerBrakeSlowdown": "hw_power_brake_slowdown",
+        "nvmlClocksEventReasonDisplayClockSetting": "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.ok = False
+        self.samples = []
+        self.reasons = set()
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.bits = {getattr(pynvml, k): v for k, v in self.NAMES.items() if hasattr(pynvml, k)}
+            self.ok = True
+        except Exception:  # NVML missing: report null clocks
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.bits.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------- oracle arms
+
+def oracle_sample_rate(n: int, modes, budget_s: float, seed: int = 0):
+    """Time the CPU oracle, as it stands, on a bounded sample of the workload:
+    R rows of every mode's n^3 problem, R calibrated to ~budget_s seconds."""
+    import numpy as np
+    import oracle
+    import synth
+    A = synth.uniform_f16(seed, synth.MATRIX_A, n, n)
+    B = synth.uniform_f16(seed, synth.MATRIX_B, n, n)
+    Cs = {m: (synth.uniform_f32 if m == "f32" else synth.uniform_f16)(seed, synth.MATRIX_C, n, n) for m in modes}
+    probe_rows = 4
+    t0 = time.perf_counter()
+    for m in modes:
+        oracle.gemm(A, B, Cs[m], rows=np.arange(probe_rows))
+    t_probe = time.perf_counter() - t0
+    rows = int(max(probe_rows, min(n, round(probe_rows * budget_s / max(t_probe, 1e-6)))))
+    sel = np.linspace(0, n - 1, rows).astype(np.int64)
+    t0 = time.perf_counter()
+    for m in modes:
+        oracle.gemm(A, B, Cs[m], rows=sel)
+    dt = time.perf_counter() - t0
+    flops = 2.0 * rows * n * n * len(modes)
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{rows} evenly spaced rows of each of the {len(modes)} M=N=K={n} problems "
+                      f"({'/'.join(modes)} acc), 2*rows*N*K flop each; {dt:.1f} s host wall clock",
+            "seconds": dt, "rows": rows}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import oracle
+    import synth
+    n = args.size
+    modes = args.modes.split(",")
+    A = synth.uniform_f16(0, synth.MATRIX_A, n, n)
+    B = synth.uniform_f16(0, synth.MATRIX_B, n, n)
+    Cs = {m: (synth.uniform_f32 if m == "f32" else synth.uniform_f16)(0, synth.MATRIX_C, n, n) for m in modes}
+    # size each step so warmup + steps fit in a few minutes
+    total_budget = 150.0
+    per_step = total_budget / max(1, args.steps + args.warmup)
+    t0 = time.perf_counter()
+    for m in modes:
+        oracle.gemm(A, B, Cs[m], rows=np.arange(2))
+    t2 = (time.perf_counter() - t0) / 2.0
+    rows = int(max(1, min(n, per_step / max(t2, 1e-6))))
+    sel = np.linspace(0, n - 1, rows).astype(np.int64)
+    for _ in range(args.warmup):
+        for m in modes:
+            oracle.gemm(A, B, Cs[m], rows=sel)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for m in modes:
+            oracle.gemm(A, B, Cs[m], rows=sel)
+    dt = time.perf_counter() - t0
+    flops = 2.0 * rows * n * n * len(modes) * args.steps
+    value = flops / dt / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded uniform[-1,1) F16 inputs)",
+        "config": {"workload": f"M=N=K={n}, F16 inputs, {'+'.join(modes)} accumulate; each step = {rows} "
+                               f"sampled rows per mode (bounded CPU sample)", "M": n, "N": n, "K": n},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": f"{rows} evenly spaced rows of each M=N=K={n} problem per step"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2108_13191_b200 as g
+
+    rank, world, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (the product path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    g.load_library()
+
+    n = args.size
+    M = N = K = n
+    modes = args.modes.split(",")
+    seed = rank  # one independent problem per GPU
+    A_h = synth.uniform_f16(seed, synth.MATRIX_A, M, K)
+    B_h = synth.uniform_f16(seed, synth.MATRIX_B, K, N)
+    C_h = {"f32": synth.uniform_f32(seed, synth.MATRIX_C, M, N), "f16": synth.uniform_f16(seed, synth.MATRIX_C, M, N)}
+    A = torch.from_numpy(A_h).to(dev)
+    B = torch.from_numpy(B_h).to(dev)
+    C = {m: torch.from_numpy(C_h[m]).to(dev) for m in modes}
+    stream = torch.cuda.Stream(dev)
+    flops = 2.0 * M * N * K
+
+    def step(ev=None):
+        for i, m in enumerate(modes):
+            if ev is not None:
+                ev[m][0].record(stream)
+            g.gemm_f16(A, B, C[m], stream=stream, config=args.config)
+            if ev is not None:
+                ev[m][1].record(stream)
+
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    ev = {m: [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)] for m in modes}
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for s in range(args.steps):
+            step({m: ev[m][s] for m in modes})
+            launches += len(modes) * g.last_launches()
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    per_mode_ms = {m: statistics.mean(ev[m][s][0].elapsed_time(ev[m][s][1]) for s in range(args.steps)) for m in modes}
+    value = world * flops * len(modes) * args.steps / (elapsed_ms * 1e-3) / 1e12
+
+    peaks = load_peaks()
+    mode_stats = {m: {"tflops": flops / (per_mode_ms[m] * 1e-3) / 1e12, "ms": per_mode_ms[m],
+                      "frac_of_2250": flops / (per_mode_ms[m] * 1e-3) / 1e12 / NOMINAL_F16_DENSE_TFLOPS,
+                      "config": g.pick_config(M, N, K, 0 if m == "f32" else 1) if args.config == "auto"
+                      else g.CONFIGS[args.config]} for m in modes}
+    dom = max(modes, key=lambda m: per_mode_ms[m])
+    achieved = mode_stats[dom]["tflops"]
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(f"{n}_{dom}")
+        except (OSError, ValueError):
+            traffic = None
+
+    # --------------------------------------------------------- e2e through the host-buffer C ABI
+    e2e = None
+    if not args.no_e2e:
+        hA = torch.from_numpy(A_h).pin_memory()
+        hB = torch.from_numpy(B_h).pin_memory()
+        hC = {m: torch.from_numpy(C_h[m].copy()).pin_memory() for m in modes}
+        dC = {m: torch.empty_like(C[m]) for m in modes}
+        dA = torch.empty_like(A)
+        dB = torch.empty_like(B)
+
+        def e2e_step():
+            for m in modes:
+                g.gemm_f16_host(hA, hB, hC[m], dA, dB, dC[m], stream=stream)
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        h2d = sum(A_h.nbytes + B_h.nbytes + C_h[m].nbytes for m in modes)
+        d2h = sum(C_h[m].nbytes for m in modes)
+        e2e = {"value": world * flops * len(modes) * args.e2e_steps / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "ms_per_step": e_ms / args.e2e_steps,
+               "path": "gemm_f16_host (C ABI): pinned host A,B,C -> H2D -> GEMM -> D2H, per mode"}
+
+    # --------------------------------------------------------- sampled parity of this launch config
+    parity = None
+    if rank == 0 and not args.no_parity:
+        import oracle
+        rows = synth.sample_rows(M, tile_m=256, n_random=0)[:: max(1, M // 256 // 8)][:12]
+        parity = {"rows": int(len(rows))}
+        ok = True
+        for m in modes:
+            Cm = torch.from_numpy(C_h[m]).to(dev)
+            g.gemm_f16(A, B, Cm, stream=stream, config=args.config)
+            torch.cuda.synchronize()
+            got = Cm[torch.from_numpy(rows).to(dev)].cpu().numpy().astype(np.float64)
+            ex, _ = oracle.gemm(A_h, B_h, C_h[m], rows=rows)
+            err = got - ex
+            rel = float(np.linalg.norm(err) / np.linalg.norm(ex))
+            parity[m] = {"rel_fro": rel, "max_abs": float(np.abs(err).max())}
+            if m == "f32":
+                bound = 1e-3 * np.sqrt(K) * float(np.abs(A_h.astype(np.float32)).max()) * float(np.abs(B_h.astype(np.float32)).max())
+                ok &= rel <= 1e-5 and parity[m]["max_abs"] <= bound
+            else:
+                ok &= rel <= 2e-3
+        parity["pass"] = bool(ok)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample_rate(n, modes, args.cpu_seconds)
+        cpu.pop("seconds", None)
+        cpu.pop("rows", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic (seeded uniform[-1,1) inputs rounded to F16; C_in uniform F32/F16)",
+            "config": {"workload": f"M=N=K={n} C+=A.B, F16 A/B row-major; one F32-acc and one F16-acc GEMM "
+                                   f"per step" if len(modes) == 2 else f"M=N=K={n}, {modes[0]} acc",
+                       "M": M, "N": N, "K": K, "modes": modes,
+                       "kernel_config": args.config,
+                       "l2": "inputs larger than L2 (A 128 MB + B 128 MB + C 256/128 MB per step > 126 MB)",
+                       "parallelism": "single GPU" if world == 1 else f"batch-one-per-GPU x{world} (no collective)"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
+                         "frac": achieved / peaks["tflops"], "traffic": traffic, "kernel": f"gemm {dom}-acc",
+                         "peak_source": peaks["source"],
+                         "frac_of_nominal_2250": achieved / NOMINAL_F16_DENSE_TFLOPS},
+            "modes": mode_stats,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

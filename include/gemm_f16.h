@@ -1,0 +1,137 @@
+/*
+ * gemm_f16.h -- C ABI of the B200 (sm_100a) tensor-core GEMM library
+ * (libgemm_f16.so), the one hot path of arXiv 2108.13191:
+ *
+ *     C[i][j] <- C[i][j] + sum_k A[i][k] * B[k][j]      0 <= i < M, 0 <= j < N
+ *
+ * PAPER.md Sec. 4: "we consider a matmul of the form C = AB + C (all
+ * three matrices are stored in a row-major layout)"; naive loop nest Sec. 3.1
+ * P:412-438; F16 inputs with F32 accumulate/output Sec. 4.1; F16
+ * inputs with F16 accumulate/output Sec. 4.2 P:976-980.  No alpha / beta.
+ *
+ * Precision (readings R3/R4): A and B are IEEE binary16.  The tensor
+ * cores accumulate in F32 in both modes; GEMM_ACC_F16 reads and writes C as
+ * binary16 and rounds once to nearest-even on output (overflow -> +-Inf).
+ *
+ * Layout: every matrix is row-major with a leading dimension in ELEMENTS
+ * (element (r,c) at ptr[r*ld + c]).  Elements of C outside the M x N window
+ * (ld padding) are never read or written.
+ *
+ * Ownership: the caller owns all buffers; the library allocates no device
+ * memory.  C must not alias A or B.  Buffers must stay valid until the work
+ * enqueued on `stream` has completed.
+ *
+ * Errors: every argument check happens before anything is enqueued, so an
+ * error status means nothing was launched.  Calls are enqueue-only
+ * (asynchronous with respect to the host); kernel faults surface at the
+ * caller's next synchronisation, as usual in CUDA.  Reentrant and thread-safe.
+ * Results are bitwise reproducible for identical inputs, shape, mode and
+ * options on the same device model (no split-K, no atomics).
+ */
+#ifndef GEMM_F16_H_
+#define GEMM_F16_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GEMM_ACC_F32 = 0, /* C is float (IEEE binary32); F32 accumulate  */
+  GEMM_ACC_F16 = 1  /* C is IEEE binary16; F16 in/out, see R3     */
+} gemm_acc_t;
+
+typedef enum {
+  GEMM_OK = 0,
+  GEMM_ERR_INVALID_VALUE = 1,      /* negative extent, short leading dim, NULL with work, bad mode/option */
+  GEMM_ERR_MISALIGNED = 2,         /* pointer not 16-byte aligned or ld*sizeof(elem) not a multiple of 16 */
+  GEMM_ERR_UNSUPPORTED_DEVICE = 3, /* current device is not compute capability 10.0 (B200, sm_100a)       */
+  GEMM_ERR_CUDA = 4                /* a CUDA runtime/driver call failed; see gemm_last_cuda_error()         */
+} gemm_status_t;
+
+/* Kernel configurations (tile = (128 * cta_group) x BN per MMA group). */
+typedef enum {
+  GEMM_CFG_AUTO = 0,
+  GEMM_CFG_PAIR_256x256 = 1, /* cta_group::2, 2-CTA cluster, UMMA 256x256x16 */
+  GEMM_CFG_PAIR_256x128 = 2, /* cta_group::2, 2-CTA cluster, UMMA 256x128x16 */
+  GEMM_CFG_SOLO_128x256 = 3, /* cta_group::1, UMMA 128x256x16               */
+  GEMM_CFG_SOLO_128x128 = 4, /* cta_group::1, UMMA 128x128x16               */
+  GEMM_CFG_SOLO_128x64 = 5,  /* cta_group::1, UMMA 128x64x16                */
+  GEMM_CFG_COUNT = 6
+} gemm_config_t;
+
+typedef struct {
+  int config;       /* gemm_config_t; GEMM_CFG_AUTO picks from the shape              */
+  int max_clusters; /* 0: one persistent cluster per resident slot; >0: cap the grid   */
+  int group_m;      /* 0: default raster group height (tiles); >0: override            */
+} gemm_options_t;
+
+/*
+ * gemm_f16: enqueue C += A.B on `stream` (cudaStream_t; NULL = legacy default).
+ *   M, N, K    extents, each in [0, 2^31-1].  M == 0 or N == 0 or K == 0:
+ *              GEMM_OK with nothing launched (K == 0 leaves C unchanged).
+ *   A, lda     device pointer, binary16, M x K row-major, lda >= max(1, K)
+ *   B, ldb     device pointer, binary16, K x N row-major, ldb >= max(1, N)
+ *   C, ldc     device pointer, float (GEMM_ACC_F32) or binary16 (GEMM_ACC_F16),
+ *              M x N row-major, ldc >= max(1, N); read (C_in) and written (C_out)
+ *   acc_type   gemm_acc_t
+ * Alignment (TMA): A, B, C 16-byte aligned; lda*2, ldb*2 and ldc*sizeof(C elem)
+ * multiples of 16 bytes, else GEMM_ERR_MISALIGNED.  There is no slow fallback.
+ */
+gemm_status_t gemm_f16(int64_t M, int64_t N, int64_t K,
+                       const void* A, int64_t lda,
+                       const void* B, int64_t ldb,
+                       void* C, int64_t ldc,
+                       int acc_type, void* stream);
+
+/* gemm_f16 with explicit options (NULL = defaults).  Same contract. */
+gemm_status_t gemm_f16_ex(int64_t M, int64_t N, int64_t K,
+                          const void* A, int64_t lda,
+                          const void* B, int64_t ldb,
+                          void* C, int64_t ldc,
+                          int acc_type, void* stream,
+                          const gemm_options_t* opts);
+
+/*
+ * gemm_f16_host: the same operation on HOST buffers (end-to-end path).
+ * Enqueues on `stream`: host->device copies of A, B and C_in into the caller's
+ * device scratch (dA/ldda, dB/lddb, dC/lddc, same element types and alignment
+ * rules as gemm_f16), the GEMM, and the device->host copy of C_out back into
+ * hC.  Host buffers should be page-locked for the copies to be asynchronous.
+ * The caller synchronises `stream` before reading hC.
+ */
+gemm_status_t gemm_f16_host(int64_t M, int64_t N, int64_t K,
+                            const void* hA, int64_t lda,
+                            const void* hB, int64_t ldb,
+                            void* hC, int64_t ldc,
+                            int acc_type,
+                            void* dA, int64_t ldda,
+                            void* dB, int64_t lddb,
+                            void* dC, int64_t lddc,
+                            void* stream);
+
+/* Configuration gemm_f16 would use for this shape (a gemm_config_t), or -1. */
+int gemm_f16_pick_config(int64_t M, int64_t N, int64_t K, int acc_type);
+
+/* Static description of a configuration: tile rows/cols, cta_group, pipeline
+ * stages, dynamic shared memory bytes.  Returns GEMM_ERR_INVALID_VALUE for an
+ * unknown config.  Pure host function (no device needed). */
+gemm_status_t gemm_f16_config_info(int config, int acc_type, int* tile_m, int* tile_n,
+                                   int* cta_group, int* stages, int* smem_bytes);
+
+/* Number of kernel launches the last successful gemm_f16* call on this host
+ * thread enqueued (0 or 1). */
+int gemm_f16_last_launches(void);
+
+const char* gemm_status_string(gemm_status_t s);
+
+/* Thread-local cudaError_t behind the last GEMM_ERR_CUDA on this thread. */
+int gemm_last_cuda_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GEMM_F16_H_ */

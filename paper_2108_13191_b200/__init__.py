@@ -1,0 +1,196 @@
+"""B200-native (sm_100a) tensor-core GEMM: C += A.B with F16 inputs, F32 or F16 C.
+
+The one hot path of arXiv 2108.13191 (Sec. 4: "C = AB + C,
+all three matrices ... row-major"; F32 accumulate P:926-930, F16 P:976-980),
+re-designed for Blackwell: a persistent, warp-specialised kernel (TMA producer,
+single-thread tcgen05.mma issuer with TMEM accumulators, epilogue warpgroup)
+behind the C ABI declared in include/gemm_f16.h.
+
+This module is argument marshalling only: torch supplies device memory and
+streams; every arithmetic step runs in libgemm_f16.so.  If the library is
+missing the import of the binding fails loudly -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import _build
+
+__all__ = ["gemm_f16", "gemm_f16_host", "GemmError", "ACC_F32", "ACC_F16", "CONFIGS",
+           "config_info", "pick_config", "library_path", "load_library", "last_launches"]
+
+ACC_F32 = 0
+ACC_F16 = 1
+CONFIGS = {
+    "auto": 0,
+    "pair_256x256": 1,
+    "pair_256x128": 2,
+    "solo_128x256": 3,
+    "solo_128x128": 4,
+    "solo_128x64": 5,
+}
+_STATUS = {0: "GEMM_OK", 1: "GEMM_ERR_INVALID_VALUE", 2: "GEMM_ERR_MISALIGNED",
+           3: "GEMM_ERR_UNSUPPORTED_DEVICE", 4: "GEMM_ERR_CUDA"}
+
+EXPORTED_SYMBOLS = ("gemm_f16", "gemm_f16_ex", "gemm_f16_host", "gemm_f16_pick_config",
+                    "gemm_f16_config_info", "gemm_f16_last_launches", "gemm_status_string",
+                    "gemm_last_cuda_error")
+
+
+class GemmError(RuntimeError):
+    def __init__(self, status: int, cuda_error: int = 0):
+        self.status = status
+        self.cuda_error = cuda_error
+        msg = _STATUS.get(status, f"status {status}")
+        if status == 4:
+            msg += f" (cudaError {cuda_error})"
+        super().__init__(msg)
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("config", ctypes.c_int), ("max_clusters", ctypes.c_int), ("group_m", ctypes.c_int)]
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def load_library(build_if_missing: bool = True):
+    """Load libgemm_f16.so (building it with nvcc if stale).  Raises if unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing:
+        try:
+            _build.build()
+        except (OSError, RuntimeError) as e:  # nvcc missing on a box with a prebuilt .so
+            if not os.path.exists(_build.LIB):
+                raise RuntimeError(f"libgemm_f16.so is missing and cannot be built: {e}") from e
+    if not os.path.exists(_build.LIB):
+        raise RuntimeError(f"libgemm_f16.so not found at {_build.LIB}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(_build.LIB)
+    i64, vp, ci = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
+    lib.gemm_f16.restype = ci
+    lib.gemm_f16.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, ci, vp]
+    lib.gemm_f16_ex.restype = ci
+    lib.gemm_f16_ex.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, ci, vp, ctypes.POINTER(_Options)]
+    lib.gemm_f16_host.restype = ci
+    lib.gemm_f16_host.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, ci, vp, i64, vp, i64, vp, i64, vp]
+    lib.gemm_f16_pick_config.restype = ci
+    lib.gemm_f16_pick_config.argtypes = [i64, i64, i64, ci]
+    lib.gemm_f16_config_info.restype = ci
+    lib.gemm_f16_config_info.argtypes = [ci, ci] + [ctypes.POINTER(ci)] * 5
+    lib.gemm_f16_last_launches.restype = ci
+    lib.gemm_f16_last_launches.argtypes = []
+    lib.gemm_status_string.restype = ctypes.c_char_p
+    lib.gemm_status_string.argtypes = [ci]
+    lib.gemm_last_cuda_error.restype = ci
+    lib.gemm_last_cuda_error.argtypes = []
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise GemmError(status, _lib.gemm_last_cuda_error() if status == 4 else 0)
+
+
+def _ld(t, name):
+    """Leading dimension (elements) of a row-major 2-D tensor with unit column stride."""
+    if t.dim() != 2:
+        raise ValueError(f"{name} must be 2-D")
+    if t.size(1) > 1 and t.stride(1) != 1:
+        raise ValueError(f"{name} must be row-major (unit column stride)")
+    if t.size(0) > 1:
+        return t.stride(0)
+    # a single row: the stride is never used to address memory, but TMA still
+    # needs a 16-byte multiple >= the row length
+    per16 = 16 // t.element_size()
+    return -(-max(t.size(1), 1) // per16) * per16
+
+
+def _stream_handle(stream, device):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _acc_of(C):
+    import torch
+    if C.dtype == torch.float32:
+        return ACC_F32
+    if C.dtype == torch.float16:
+        return ACC_F16
+    raise TypeError(f"C must be float32 (F32 accumulate) or float16 (F16), got {C.dtype}")
+
+
+def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int = 0):
+    """In place: C += A @ B on the GPU (enqueued on `stream`, default: torch's current).
+
+    A: (M, K) torch.float16 CUDA, B: (K, N) torch.float16 CUDA, C: (M, N) float32 or
+    float16 CUDA; all row-major with unit column stride (row strides = leading dims).
+    config: a name in CONFIGS or its id (0 = auto).  Raises GemmError on a non-zero status.
+    """
+    import torch
+    lib = load_library()
+    for name, t in (("A", A), ("B", B), ("C", C)):
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if A.dtype != torch.float16 or B.dtype != torch.float16:
+        raise TypeError("A and B must be torch.float16")
+    acc = _acc_of(C)
+    M, K = A.shape
+    K2, N = B.shape
+    if K2 != K or tuple(C.shape) != (M, N):
+        raise ValueError(f"shape mismatch: A{tuple(A.shape)} B{tuple(B.shape)} C{tuple(C.shape)}")
+    cfg = CONFIGS[config] if isinstance(config, str) else int(config)
+    opts = _Options(cfg, int(max_clusters), int(group_m))
+    with torch.cuda.device(C.device):
+        st = lib.gemm_f16_ex(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
+                             C.data_ptr(), _ld(C, "C"), acc, _stream_handle(stream, C.device),
+                             ctypes.byref(opts))
+    _check(st)
+    return C
+
+
+def gemm_f16_host(hA, hB, hC, dA, dB, dC, stream=None):
+    """End-to-end path: host (pinned) A, B, C -> device scratch -> GEMM -> C back to host.
+
+    hA/hB/hC are CPU torch tensors (float16 / float16 / float32|float16); dA/dB/dC
+    are CUDA scratch tensors of the same shapes and dtypes.  Enqueued on `stream`;
+    the caller synchronises before reading hC.
+    """
+    import torch
+    lib = load_library()
+    acc = _acc_of(hC)
+    M, K = hA.shape
+    _, N = hB.shape
+    with torch.cuda.device(dC.device):
+        st = lib.gemm_f16_host(M, N, K, hA.data_ptr(), _ld(hA, "hA"), hB.data_ptr(), _ld(hB, "hB"),
+                               hC.data_ptr(), _ld(hC, "hC"), acc,
+                               dA.data_ptr(), _ld(dA, "dA"), dB.data_ptr(), _ld(dB, "dB"),
+                               dC.data_ptr(), _ld(dC, "dC"), _stream_handle(stream, dC.device))
+    _check(st)
+    return hC
+
+
+def pick_config(M: int, N: int, K: int, acc: int = ACC_F32) -> int:
+    return int(load_library().gemm_f16_pick_config(M, N, K, acc))
+
+
+def config_info(config, acc: int = ACC_F32) -> dict:
+    lib = load_library()
+    cfg = CONFIGS[config] if isinstance(config, str) else int(config)
+    vals = [ctypes.c_int() for _ in range(5)]
+    _check(lib.gemm_f16_config_info(cfg, acc, *[ctypes.byref(v) for v in vals]))
+    keys = ("tile_m", "tile_n", "cta_group", "stages", "smem_bytes")
+    return {k: v.value for k, v in zip(keys, vals)}
+
+
+def last_launches() -> int:
+    return int(load_library().gemm_f16_last_launches())

@@ -1,0 +1,340 @@
+// gemm_api.cu -- host side of libgemm_f16.so (B2): argument validation,
+// per-device capability cache, CUtensorMap encoding, configuration choice and
+// cudaLaunchKernelEx with cluster dimensions.  Contract: include/gemm_f16.h.
+//
+// Replaces the paper's host path (Sec. 3.11: gpu.launch ->
+// MLIR CUDA runtime wrappers, JIT via mlir-cpu-runner) with an AOT-compiled
+// sm_100a library; the tile-configuration choice plays the role of the
+// paper's per-size "best performing version".
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/gemm_f16.h"
+#include "gemm_sm100.cuh"
+
+namespace {
+
+using namespace g16;
+
+thread_local int t_last_cuda_error = 0;
+thread_local int t_last_launches = 0;
+
+using Cfg1F32 = KCfg<2, 256, 6, false>;
+using Cfg1F16 = KCfg<2, 256, 6, true>;
+using Cfg2F32 = KCfg<2, 128, 8, false>;
+using Cfg2F16 = KCfg<2, 128, 8, true>;
+using Cfg3F32 = KCfg<1, 256, 4, false>;
+using Cfg3F16 = KCfg<1, 256, 4, true>;
+using Cfg4F32 = KCfg<1, 128, 6, false>;
+using Cfg4F16 = KCfg<1, 128, 6, true>;
+using Cfg5F32 = KCfg<1, 64, 8, false>;
+using Cfg5F16 = KCfg<1, 64, 8, true>;
+
+using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const GemmParams);
+
+struct ConfigDesc {
+  int cta_group, tile_n, stages, smem[2];
+  KernelFn fn[2];  // [acc_type]
+};
+
+template <class C32, class C16>
+constexpr ConfigDesc make_desc() {
+  return ConfigDesc{C32::CG, C32::BN, C32::STAGES, {C32::SMEM_BYTES, C16::SMEM_BYTES},
+                    {&gemm_f16_sm100_kernel<C32>, &gemm_f16_sm100_kernel<C16>}};
+}
+
+const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
+    ConfigDesc{0, 0, 0, {0, 0}, {nullptr, nullptr}},
+    make_desc<Cfg1F32, Cfg1F16>(),
+    make_desc<Cfg2F32, Cfg2F16>(),
+    make_desc<Cfg3F32, Cfg3F16>(),
+    make_desc<Cfg4F32, Cfg4F16>(),
+    make_desc<Cfg5F32, Cfg5F16>(),
+};
+
+// ---------------------------------------------------------------- device cache
+constexpr int kMaxDevices = 64;
+struct DeviceInfo {
+  gemm_status_t status = GEMM_OK;
+  int cuda_error = 0;
+  int sm_count = 0;
+  int max_clusters[GEMM_CFG_COUNT][2] = {};
+};
+std::once_flag g_dev_once[kMaxDevices];
+DeviceInfo g_dev[kMaxDevices];
+
+void init_device(int dev) {
+  DeviceInfo& d = g_dev[dev];
+  int major = 0, minor = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
+  if (major != 10 || minor != 0) { d.status = GEMM_ERR_UNSUPPORTED_DEVICE; return; }
+  for (int c = 1; c < GEMM_CFG_COUNT; ++c) {
+    for (int a = 0; a < 2; ++a) {
+      const ConfigDesc& cd = kConfigs[c];
+      e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.fn[a]),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, cd.smem[a]);
+      if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
+      if (cd.cta_group == 2) {
+        e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.fn[a]),
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+        cudaLaunchConfig_t lc = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        lc.gridDim = dim3(2 * (d.sm_count / 2), 1, 1);
+        lc.blockDim = dim3(256, 1, 1);
+        lc.dynamicSmemBytes = cd.smem[a];
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+        int n = 0;
+        e = cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(cd.fn[a]), &lc);
+        if (e != cudaSuccess || n <= 0) { d.status = GEMM_ERR_CUDA; d.cuda_error = e ? e : cudaErrorInvalidConfiguration; return; }
+        d.max_clusters[c][a] = n;
+      } else {
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cd.fn[a], 256, cd.smem[a]);
+        if (e != cudaSuccess || per_sm <= 0) { d.status = GEMM_ERR_CUDA; d.cuda_error = e ? e : cudaErrorInvalidConfiguration; return; }
+        d.max_clusters[c][a] = per_sm * d.sm_count;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- tensor maps
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode_fn() {
+  static PFN_encodeTiled fn = []() -> PFN_encodeTiled {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<PFN_encodeTiled>(p);
+  }();
+  return fn;
+}
+
+// 2-D row-major tensor (rows x cols, ld elements), box = box_cols x box_rows, 128B swizzle.
+bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* ptr, int64_t rows,
+               int64_t cols, int64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapL2promotion l2) {
+  PFN_encodeTiled enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esize};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int pick_config(int64_t M, int64_t N, int sm_count) {
+  const int64_t pair_slots = sm_count / 2;
+  if (cdiv(M, 256) * cdiv(N, 256) >= pair_slots) return GEMM_CFG_PAIR_256x256;
+  if (cdiv(M, 256) * cdiv(N, 128) >= pair_slots) return GEMM_CFG_PAIR_256x128;
+  if (cdiv(M, 128) * cdiv(N, 128) >= sm_count) return GEMM_CFG_SOLO_128x128;
+  return GEMM_CFG_SOLO_128x64;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+gemm_status_t cuda_fail(cudaError_t e) {
+  t_last_cuda_error = static_cast<int>(e);
+  return GEMM_ERR_CUDA;
+}
+
+gemm_status_t validate(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb,
+                       const void* C, int64_t ldc, int acc_type, bool* no_work) {
+  const int64_t kMax = 0x7fffffffLL;
+  if (M < 0 || N < 0 || K < 0 || M > kMax || N > kMax || K > kMax) return GEMM_ERR_INVALID_VALUE;
+  if (acc_type != GEMM_ACC_F32 && acc_type != GEMM_ACC_F16) return GEMM_ERR_INVALID_VALUE;
+  if (lda < std::max<int64_t>(1, K) || ldb < std::max<int64_t>(1, N) || ldc < std::max<int64_t>(1, N))
+    return GEMM_ERR_INVALID_VALUE;
+  *no_work = (M == 0 || N == 0 || K == 0);
+  if (*no_work) return GEMM_OK;
+  if (!A || !B || !C) return GEMM_ERR_INVALID_VALUE;
+  const int64_t csz = acc_type == GEMM_ACC_F32 ? 4 : 2;
+  if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return GEMM_ERR_MISALIGNED;
+  if ((lda * 2) % 16 || (ldb * 2) % 16 || (ldc * csz) % 16) return GEMM_ERR_MISALIGNED;
+  if (lda * 2 >= (int64_t(1) << 40) || ldb * 2 >= (int64_t(1) << 40) || ldc * csz >= (int64_t(1) << 40))
+    return GEMM_ERR_INVALID_VALUE;
+  return GEMM_OK;
+}
+
+gemm_status_t device_ready(int* dev_out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (dev < 0 || dev >= kMaxDevices) return GEMM_ERR_UNSUPPORTED_DEVICE;
+  std::call_once(g_dev_once[dev], init_device, dev);
+  if (g_dev[dev].status == GEMM_ERR_CUDA) {
+    t_last_cuda_error = g_dev[dev].cuda_error;
+    return GEMM_ERR_CUDA;
+  }
+  *dev_out = dev;
+  return g_dev[dev].status;
+}
+
+gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb,
+                     void* C, int64_t ldc, int acc_type, cudaStream_t stream, const gemm_options_t* opts) {
+  int dev = 0;
+  gemm_status_t st = device_ready(&dev);
+  if (st != GEMM_OK) return st;
+  const DeviceInfo& di = g_dev[dev];
+
+  int cfg = opts ? opts->config : GEMM_CFG_AUTO;
+  if (cfg < 0 || cfg >= GEMM_CFG_COUNT) return GEMM_ERR_INVALID_VALUE;
+  if (cfg == GEMM_CFG_AUTO) cfg = pick_config(M, N, di.sm_count);
+  const ConfigDesc& cd = kConfigs[cfg];
+  const int a = acc_type;
+
+  CUtensorMap tm_a, tm_b, tm_c;
+  const bool ok =
+      encode_2d(&tm_a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, A, M, K, lda, 64, 128, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
+      encode_2d(&tm_b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, B, K, N, ldb, 64, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
+      (acc_type == GEMM_ACC_F32
+           ? encode_2d(&tm_c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, M, N, ldc, 32, 32,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B)
+           : encode_2d(&tm_c, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, C, M, N, ldc, 64, 32,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B));
+  if (!ok) return cuda_fail(cudaErrorInvalidValue);
+
+  GemmParams p;
+  p.M = static_cast<int>(M);
+  p.N = static_cast<int>(N);
+  p.K = static_cast<int>(K);
+  const int tile_m = 128 * cd.cta_group;
+  p.tiles_m = static_cast<int>(cdiv(M, tile_m));
+  p.tiles_n = static_cast<int>(cdiv(N, cd.tile_n));
+  const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n;
+  if (tiles > 0x7fffffffLL) return GEMM_ERR_INVALID_VALUE;
+  p.num_tiles = static_cast<int>(tiles);
+  p.k_blocks = static_cast<int>(cdiv(K, 64));
+  p.group_m = (opts && opts->group_m > 0) ? opts->group_m : 8;
+  if (opts && opts->group_m < 0) return GEMM_ERR_INVALID_VALUE;
+  const int64_t csize = acc_type == GEMM_ACC_F32 ? 4 : 2;
+  p.c_ragged = (N * csize) % 16 != 0;
+  p.c_ptr = C;
+  p.ldc = ldc;
+
+  int clusters = di.max_clusters[cfg][a];
+  if (opts && opts->max_clusters > 0) clusters = std::min(clusters, opts->max_clusters);
+  if (opts && opts->max_clusters < 0) return GEMM_ERR_INVALID_VALUE;
+  clusters = static_cast<int>(std::min<int64_t>(clusters, tiles));
+
+  cudaLaunchConfig_t lc = {};
+  cudaLaunchAttribute attr[1];
+  lc.gridDim = dim3(static_cast<unsigned>(clusters * cd.cta_group), 1, 1);
+  lc.blockDim = dim3(256, 1, 1);
+  lc.dynamicSmemBytes = cd.smem[a];
+  lc.stream = stream;
+  if (cd.cta_group == 2) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&lc, cd.fn[a], tm_a, tm_b, tm_c, p);
+  if (e != cudaSuccess) return cuda_fail(e);
+  t_last_launches = 1;
+  return GEMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+gemm_status_t gemm_f16_ex(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb,
+                          void* C, int64_t ldc, int acc_type, void* stream, const gemm_options_t* opts) {
+  t_last_launches = 0;
+  bool no_work = false;
+  gemm_status_t st = validate(M, N, K, A, lda, B, ldb, C, ldc, acc_type, &no_work);
+  if (st != GEMM_OK || no_work) return st;
+  return launch(M, N, K, A, lda, B, ldb, C, ldc, acc_type, static_cast<cudaStream_t>(stream), opts);
+}
+
+gemm_status_t gemm_f16(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb,
+                       void* C, int64_t ldc, int acc_type, void* stream) {
+  return gemm_f16_ex(M, N, K, A, lda, B, ldb, C, ldc, acc_type, stream, nullptr);
+}
+
+gemm_status_t gemm_f16_host(int64_t M, int64_t N, int64_t K, const void* hA, int64_t lda, const void* hB,
+                            int64_t ldb, void* hC, int64_t ldc, int acc_type, void* dA, int64_t ldda, void* dB,
+                            int64_t lddb, void* dC, int64_t lddc, void* stream) {
+  t_last_launches = 0;
+  bool no_work = false;
+  gemm_status_t st = validate(M, N, K, dA, ldda, dB, lddb, dC, lddc, acc_type, &no_work);
+  if (st != GEMM_OK || no_work) return st;
+  if (!hA || !hB || !hC) return GEMM_ERR_INVALID_VALUE;
+  if (lda < std::max<int64_t>(1, K) || ldb < std::max<int64_t>(1, N) || ldc < std::max<int64_t>(1, N))
+    return GEMM_ERR_INVALID_VALUE;
+  int dev = 0;
+  st = device_ready(&dev);
+  if (st != GEMM_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t csz = acc_type == GEMM_ACC_F32 ? 4 : 2;
+  cudaError_t e = cudaMemcpy2DAsync(dA, ldda * 2, hA, lda * 2, K * 2, M, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(dB, lddb * 2, hB, ldb * 2, N * 2, K, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(dC, lddc * csz, hC, ldc * csz, N * csz, M, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e);
+  st = launch(M, N, K, dA, ldda, dB, lddb, dC, lddc, acc_type, s, nullptr);
+  if (st != GEMM_OK) return st;
+  e = cudaMemcpy2DAsync(hC, ldc * csz, dC, lddc * csz, N * csz, M, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return GEMM_OK;
+}
+
+int gemm_f16_pick_config(int64_t M, int64_t N, int64_t K, int acc_type) {
+  (void)K;
+  if (acc_type != GEMM_ACC_F32 && acc_type != GEMM_ACC_F16) return -1;
+  int dev = 0;
+  if (device_ready(&dev) != GEMM_OK) return -1;
+  return pick_config(M, N, g_dev[dev].sm_count);
+}
+
+gemm_status_t gemm_f16_config_info(int config, int acc_type, int* tile_m, int* tile_n, int* cta_group, int* stages,
+                                   int* smem_bytes) {
+  if (config <= 0 || config >= GEMM_CFG_COUNT) return GEMM_ERR_INVALID_VALUE;
+  if (acc_type != GEMM_ACC_F32 && acc_type != GEMM_ACC_F16) return GEMM_ERR_INVALID_VALUE;
+  const ConfigDesc& cd = kConfigs[config];
+  if (tile_m) *tile_m = 128 * cd.cta_group;
+  if (tile_n) *tile_n = cd.tile_n;
+  if (cta_group) *cta_group = cd.cta_group;
+  if (stages) *stages = cd.stages;
+  if (smem_bytes) *smem_bytes = cd.smem[acc_type];
+  return GEMM_OK;
+}
+
+int gemm_f16_last_launches(void) { return t_last_launches; }
+
+const char* gemm_status_string(gemm_status_t s) {
+  switch (s) {
+    case GEMM_OK: return "GEMM_OK";
+    case GEMM_ERR_INVALID_VALUE: return "GEMM_ERR_INVALID_VALUE";
+    case GEMM_ERR_MISALIGNED: return "GEMM_ERR_MISALIGNED";
+    case GEMM_ERR_UNSUPPORTED_DEVICE: return "GEMM_ERR_UNSUPPORTED_DEVICE";
+    case GEMM_ERR_CUDA: return "GEMM_ERR_CUDA";
+  }
+  return "GEMM_ERR_UNKNOWN";
+}
+
+int gemm_last_cuda_error(void) { return t_last_cuda_error; }
+
+}  // extern "C"

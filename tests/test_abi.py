@@ -1,0 +1,95 @@
+"""CPU-only checks of the C-ABI library: it loads without a GPU, exports every
+symbol include/gemm_f16.h declares, and rejects bad arguments before touching
+a device (argument errors never need CUDA; no compute call is made here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2108_13191_b200 as g
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    with open(os.path.join(ROOT, "include", "gemm_f16.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"^\s*(?:gemm_status_t|int|const char\*)\s+(\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_expected_api():
+    names = _declared_functions()
+    assert set(names) == set(g.EXPORTED_SYMBOLS), names
+
+
+def test_library_loads_and_exports_every_symbol():
+    lib = g.load_library()
+    for name in _declared_functions():
+        assert hasattr(lib, name), name
+    out = os.popen(f"nm -D --defined-only {g.library_path()}").read()
+    for name in _declared_functions():
+        assert re.search(rf"\bT {name}$", out, re.M), name
+
+
+def test_status_strings():
+    lib = g.load_library()
+    for s, name in ((0, b"GEMM_OK"), (1, b"GEMM_ERR_INVALID_VALUE"), (2, b"GEMM_ERR_MISALIGNED"),
+                    (3, b"GEMM_ERR_UNSUPPORTED_DEVICE"), (4, b"GEMM_ERR_CUDA")):
+        assert lib.gemm_status_string(s) == name
+
+
+def _call(M, N, K, A=16, lda=None, B=16, ldb=None, C=16, ldc=None, acc=0):
+    lib = g.load_library()
+    lda = K if lda is None else lda
+    ldb = N if ldb is None else ldb
+    ldc = N if ldc is None else ldc
+    return lib.gemm_f16(M, N, K, A, lda, B, ldb, C, ldc, acc, None)
+
+
+def test_argument_errors_without_gpu():
+    # negative extents, short leading dims, bad mode, NULL with work: INVALID_VALUE
+    assert _call(-1, 8, 8) == 1
+    assert _call(8, -1, 8) == 1
+    assert _call(8, 8, -1) == 1
+    assert _call(8, 8, 8, lda=4) == 1
+    assert _call(8, 8, 8, ldb=4) == 1
+    assert _call(8, 8, 8, ldc=4) == 1
+    assert _call(8, 8, 8, acc=2) == 1
+    assert _call(8, 8, 8, A=0) == 1
+    assert _call(1 << 31, 8, 8) == 1
+    # misaligned pointers / leading dims: MISALIGNED
+    assert _call(8, 8, 8, A=18) == 2
+    assert _call(8, 8, 12) == 2                 # lda*2 = 24 bytes
+    assert _call(8, 12, 8, ldb=12, ldc=12) == 2 # ldb*2 = 24 bytes
+    assert _call(8, 6, 8, ldb=8, ldc=6) == 2    # F32 ldc*4 = 24 bytes
+    # quick returns: nothing launched, no device needed
+    assert _call(0, 8, 8) == 0 and g.last_launches() == 0
+    assert _call(8, 0, 8, ldb=8, ldc=8) == 0
+    assert _call(8, 8, 0, lda=8) == 0
+
+
+def test_config_info_is_host_only():
+    for name, cid in g.CONFIGS.items():
+        if cid == 0:
+            continue
+        for acc in (0, 1):
+            info = g.config_info(cid, acc)
+            assert info["tile_m"] == 128 * info["cta_group"]
+            assert info["smem_bytes"] <= 232448
+            assert info["stages"] >= 4
+    with pytest.raises(g.GemmError):
+        g.config_info(0)
+    with pytest.raises(g.GemmError):
+        g.config_info(99)
+
+
+def test_product_path_does_not_import_oracle():
+    # the product package must never reach the oracle (no CPU fallback)
+    pkg = os.path.join(ROOT, "paper_2108_13191_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h", ".c")):
+                with open(os.path.join(dirpath, fn)) as f:
+                    src = f.read()
+                assert not re.search(r"\bimport\s+oracle\b|from\s+oracle\b|liboracle", src), fn

@@ -1,0 +1,200 @@
+"""GPU parity: the CUDA path (libgemm_f16.so through the Python binding over the C ABI)
+against the CPU oracle, element by element on the same seeded inputs.
+
+Bars (BASELINE.json north_star, restated in tests/parity.py): F32 accumulate
+max|err| <= 1e-3 sqrt(K) max|A| max|B| and rel-Frobenius <= 1e-5; F16
+rel-Frobenius <= 2e-3.  Closed forms are bit-exact.  PAPER.md P:908-909.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity import Guarded, check, device_problem, oracle_full, round_up, stats
+
+pytestmark = pytest.mark.gpu
+
+CFGS = ["pair_256x256", "pair_256x128", "solo_128x256", "solo_128x128", "solo_128x64"]
+
+
+@pytest.fixture(scope="module")
+def g():
+    import torch
+    import paper_2108_13191_b200 as g
+    assert torch.cuda.is_available()
+    g.load_library()
+    return g
+
+
+def _run(g, gA, gB, gC, **kw):
+    import torch
+    g.gemm_f16(gA.view, gB.view, gC.view, **kw)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+def test_smoke_256_cube(g, acc):
+    M = N = K = 256
+    A, B, C, gA, gB, gC = device_problem(M, N, K, acc, seed=0)
+    _run(g, gA, gB, gC)
+    ex, _ = oracle_full(A, B, C)
+    check(gC.result(), ex, A, B, acc, K, "256^3 auto")
+    assert gC.guard_intact()
+
+
+@pytest.mark.parametrize("cfg", CFGS)
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+def test_configs_ragged_multi_tile(g, cfg, acc):
+    # several tiles in M and N, ragged M/N/K tails, padded leading dims
+    M, N, K = 601, 712, 333
+    A, B, C, gA, gB, gC = device_problem(M, N, K, acc, seed=1, pad=(8, 16, 8))
+    _run(g, gA, gB, gC, config=cfg)
+    ex, _ = oracle_full(A, B, C)
+    check(gC.result(), ex, A, B, acc, K, f"{cfg} {acc}")
+    assert gC.guard_intact(), "write outside the M x N window"
+    assert gA.guard_intact() and gB.guard_intact()
+
+
+@pytest.mark.parametrize("cfg", CFGS)
+def test_persistent_loop_phase_wrap(g, cfg):
+    # one cluster walks every tile: exercises ring/TMEM phase bits across many tiles
+    M, N, K = 1100, 900, 640
+    A, B, C, gA, gB, gC = device_problem(M, N, K, "f32", seed=2)
+    _run(g, gA, gB, gC, config=cfg, max_clusters=1)
+    ex, _ = oracle_full(A, B, C)
+    check(gC.result(), ex, A, B, "f32", K, f"{cfg} one cluster")
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+def test_closed_forms_bit_exact(g, acc):
+    import torch
+    # identity: A = I (M = K), C_in = 0 -> C = B exactly
+    K, N = 384, 320
+    B = synth.uniform_f16(3, 1, K, N)
+    dt = np.float32 if acc == "f32" else np.float16
+    gA = Guarded(np.eye(K, dtype=np.float16), K)
+    gB = Guarded(B, N)
+    gC = Guarded(np.zeros((K, N), dt), N)
+    _run(g, gA, gB, gC)
+    assert np.array_equal(gC.result().astype(np.float64), B.astype(np.float64))
+    # all ones: C = K (F32 exact for any K <= 2^24; F16 exact for K <= 2048)
+    for K in (16, 1000, 2048):
+        M, N = 130, 200
+        gA = Guarded(np.ones((M, K), np.float16), K)
+        gB = Guarded(np.ones((K, N), np.float16), N)
+        gC = Guarded(np.zeros((M, N), dt), N)
+        _run(g, gA, gB, gC)
+        assert np.all(gC.result() == K), K
+    # A = 0 leaves C bitwise unchanged
+    A, Bm, C, gA, gB, gC = device_problem(200, 136, 96, acc, seed=4)
+    gA.full.zero_()
+    _run(g, gA, gB, gC)
+    assert np.array_equal(gC.result().view(np.uint8), C.view(np.uint8))
+
+
+def test_small_integers_exact_f32(g):
+    rng = np.random.default_rng(11)
+    M, N, K = 520, 392, 700
+    Ai = rng.integers(-2, 3, size=(M, K))
+    Bi = rng.integers(-2, 3, size=(K, N))
+    Ci = rng.integers(-50, 51, size=(M, N))
+    gA = Guarded(Ai.astype(np.float16), round_up(K, 8))
+    gB = Guarded(Bi.astype(np.float16), N)
+    gC = Guarded(Ci.astype(np.float32), N)
+    for cfg in CFGS:
+        gC.full.copy_(__import__("torch").from_numpy(gC.full_host.copy()))
+        _run(g, gA, gB, gC, config=cfg)
+        assert np.array_equal(gC.result().astype(np.int64), Ai @ Bi + Ci), cfg
+
+
+def test_permutation_rows(g):
+    K, N = 256, 264
+    perm = np.random.default_rng(9).permutation(K)
+    P = np.zeros((K, K), np.float16)
+    P[np.arange(K), perm] = 1
+    B = synth.uniform_f16(0, 1, K, N)
+    gA, gB, gC = Guarded(P, K), Guarded(B, N), Guarded(np.zeros((K, N), np.float32), N)
+    _run(g, gA, gB, gC, config="pair_256x256")
+    assert np.array_equal(gC.result(), B.astype(np.float32)[perm])
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+def test_brute_force_tiny_shapes(g, acc):
+    rng = np.random.default_rng(5)
+    shapes = [(1, 1, 1), (1, 8, 1), (7, 9, 15), (33, 40, 17), (40, 1, 40), (2, 3, 64), (17, 24, 65)]
+    shapes += [tuple(int(x) for x in rng.integers(1, 41, size=3)) for _ in range(12)]
+    for (M, N, K) in shapes:
+        A, B, C, gA, gB, gC = device_problem(M, N, K, acc, seed=M + N + K, pad=(8, 8, 8))
+        _run(g, gA, gB, gC)
+        ex, _ = oracle_full(A, B, C)
+        check(gC.result(), ex, A, B, acc, K, f"{(M, N, K)}")
+        assert gC.guard_intact(), (M, N, K)
+
+
+def test_deterministic_and_schedule_independent(g):
+    import torch
+    M, N, K = 1024, 768, 512
+    A, B, C, gA, gB, gC = device_problem(M, N, K, "f32", seed=6)
+    outs = []
+    for mc in (0, 0, 3):
+        gC.full.copy_(torch.from_numpy(gC.full_host.copy()))
+        _run(g, gA, gB, gC, config="pair_256x256", max_clusters=mc)
+        outs.append(gC.result().copy())
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    assert np.array_equal(outs[0].view(np.uint32), outs[2].view(np.uint32))
+
+
+def test_rounding_probe_reports(g, capsys):
+    """P4: k16 block 0 contributes 1, block 1 contributes 3*2^-25.
+    RNE accumulation gives 1 + 2^-23, truncation gives 1.  Reported, and the F32
+    tolerance must hold either way."""
+    K = 32
+    A = np.zeros((128, K), np.float16)
+    B = np.zeros((K, 128), np.float16)
+    A[0, 0] = 1.0
+    B[0, 0] = 1.0
+    for k in (16, 17, 18):
+        A[0, k] = 2.0 ** -12
+        B[k, 0] = 2.0 ** -13
+    gA, gB, gC = Guarded(A, K), Guarded(B, 128), Guarded(np.zeros((128, 128), np.float32), 128)
+    _run(g, gA, gB, gC)
+    v = float(gC.result()[0, 0])
+    mode = "RNE-like" if v == 1.0 + 2.0 ** -23 else ("truncating" if v == 1.0 else f"other ({v!r})")
+    print(f"F32 accumulate rounding probe: {mode}")
+    assert v in (1.0, 1.0 + 2.0 ** -23)
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+def test_host_buffer_e2e_path(g, acc):
+    import torch
+    M, N, K = 300, 264, 200
+    A, B, C = synth.problem(M, N, K, acc, seed=8)
+    hA = torch.from_numpy(A).pin_memory()
+    hB = torch.from_numpy(B).pin_memory()
+    hC = torch.from_numpy(C.copy()).pin_memory()
+    dA = torch.empty((M, round_up(K, 8)), dtype=torch.float16, device="cuda")[:, :K]
+    dB = torch.empty((K, N), dtype=torch.float16, device="cuda")
+    dC = torch.empty((M, N), dtype=hC.dtype, device="cuda")
+    g.gemm_f16_host(hA, hB, hC, dA, dB, dC)
+    torch.cuda.synchronize()
+    ex, _ = oracle_full(A, B, C)
+    check(hC.numpy(), ex, A, B, acc, K, "host path")
+
+
+def test_errors_are_reported(g):
+    import torch
+    A = torch.zeros((64, 64), dtype=torch.float16, device="cuda")
+    B = torch.zeros((64, 64), dtype=torch.float16, device="cuda")
+    C = torch.zeros((64, 64), dtype=torch.float32, device="cuda")
+    big = torch.zeros(64 * 64 + 8, dtype=torch.float16, device="cuda")
+    misA = big[1:1 + 64 * 64].view(64, 64)
+    with pytest.raises(g.GemmError) as e:
+        g.gemm_f16(misA, B, C)
+    assert e.value.status == 2
+    with pytest.raises(g.GemmError) as e:
+        g.gemm_f16(A, B, C, config=99)
+    assert e.value.status == 1
+    # K == 0: nothing launched, C unchanged
+    C0 = C.clone()
+    g.gemm_f16(A[:, :0], B[:0, :], C)
+    assert g.last_launches() == 0 and torch.equal(C, C0)
