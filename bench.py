@@ -47,6 +47,10 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", choices=["batch", "nshard"], default="batch",
+                    help="batch: one independent n^3 problem per GPU (weak scaling, default); "
+                         "nshard: one n^3 problem N-sharded over the GPUs (strong scaling, BASELINE configs[3])")
+    ap.add_argument("--allgather", action="store_true", help="nshard: also time the NCCL all-gather of C")
     return ap.parse_args()
 
 
@@ -145,12 +149,16 @@ def oracle_sample_rate(n: int, modes, budget_s: float, seed: int = 0):
     A = synth.uniform_f16(seed, synth.MATRIX_A, n, n)
     B = synth.uniform_f16(seed, synth.MATRIX_B, n, n)
     Cs = {m: (synth.uniform_f32 if m == "f32" else synth.uniform_f16)(seed, synth.MATRIX_C, n, n) for m in modes}
-    probe_rows = 4
-    t0 = time.perf_counter()
-    for m in modes:
-        oracle.gemm(A, B, Cs[m], rows=np.arange(probe_rows))
-    t_probe = time.perf_counter() - t0
-    rows = int(max(probe_rows, min(n, round(probe_rows * budget_s / max(t_probe, 1e-6)))))
+    # t(rows) ~ a + b*rows (a: decoding B once per call); fit from two probes
+    ts = []
+    for probe_rows in (2, 8):
+        t0 = time.perf_counter()
+        for m in modes:
+            oracle.gemm(A, B, Cs[m], rows=np.arange(probe_rows))
+        ts.append(time.perf_counter() - t0)
+    b = max((ts[1] - ts[0]) / 6.0, 1e-6)
+    a = max(ts[0] - 2 * b, 0.0)
+    rows = int(max(2, min(n, (budget_s - a) / b)))
     sel = np.linspace(0, n - 1, rows).astype(np.int64)
     t0 = time.perf_counter()
     for m in modes:
@@ -236,15 +244,26 @@ def main():
     n = args.size
     M = N = K = n
     modes = args.modes.split(",")
-    seed = rank  # one independent problem per GPU
+    nshard = args.workload == "nshard"
+    if nshard:
+        from paper_2108_13191_b200 import dist as gdist
+        seed = 0
+        slabs = gdist.column_slabs(N, world, align=8)
+        n0, n1 = slabs[rank]
+    else:
+        seed = rank  # one independent problem per GPU
+        n0, n1 = 0, N
+    nr = n1 - n0
     A_h = synth.uniform_f16(seed, synth.MATRIX_A, M, K)
-    B_h = synth.uniform_f16(seed, synth.MATRIX_B, K, N)
-    C_h = {"f32": synth.uniform_f32(seed, synth.MATRIX_C, M, N), "f16": synth.uniform_f16(seed, synth.MATRIX_C, M, N)}
+    B_h = synth.uniform_f16(seed, synth.MATRIX_B, K, N, col_lo=n0, col_hi=n1)
+    C_h = {"f32": synth.uniform_f32(seed, synth.MATRIX_C, M, N, col_lo=n0, col_hi=n1),
+           "f16": synth.uniform_f16(seed, synth.MATRIX_C, M, N, col_lo=n0, col_hi=n1)}
     A = torch.from_numpy(A_h).to(dev)
     B = torch.from_numpy(B_h).to(dev)
     C = {m: torch.from_numpy(C_h[m]).to(dev) for m in modes}
     stream = torch.cuda.Stream(dev)
-    flops = 2.0 * M * N * K
+    flops = 2.0 * M * nr * K          # this rank's FLOPs per GEMM
+    job_flops = 2.0 * M * N * K * (1 if nshard else world)   # whole job, per GEMM mode
 
     def step(ev=None):
         for i, m in enumerate(modes):
@@ -281,7 +300,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
     per_mode_ms = {m: statistics.mean(ev[m][s][0].elapsed_time(ev[m][s][1]) for s in range(args.steps)) for m in modes}
-    value = world * flops * len(modes) * args.steps / (elapsed_ms * 1e-3) / 1e12
+    value = job_flops * len(modes) * args.steps / (elapsed_ms * 1e-3) / 1e12
 
     peaks = load_peaks()
     mode_stats = {m: {"tflops": flops / (per_mode_ms[m] * 1e-3) / 1e12, "ms": per_mode_ms[m],
@@ -330,10 +349,29 @@ def main():
             e_ms = float(t.item())
         h2d = sum(A_h.nbytes + B_h.nbytes + C_h[m].nbytes for m in modes)
         d2h = sum(C_h[m].nbytes for m in modes)
-        e2e = {"value": world * flops * len(modes) * args.e2e_steps / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+        e2e = {"value": job_flops * len(modes) * args.e2e_steps / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "ms_per_step": e_ms / args.e2e_steps,
                "path": "gemm_f16_host (C ABI): pinned host A,B,C -> H2D -> GEMM -> D2H, per mode"}
+
+    # --------------------------------------------------------- optional NCCL all-gather of C (nshard)
+    gather = None
+    if nshard and args.allgather and world > 1:
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        gdist.allgather_c(C[modes[0]], slabs, layout="slabs")
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0.record()
+        for m in modes:
+            gdist.allgather_c(C[m], slabs, layout="slabs")
+        g1.record()
+        torch.cuda.synchronize()
+        gms = torch.tensor([g0.elapsed_time(g1)], device=dev, dtype=torch.float64)
+        dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+        gbytes = sum(M * N * C[m].element_size() for m in modes)
+        gather = {"ms_per_step": float(gms.item()), "bytes_gathered_per_step": gbytes,
+                  "e2e_tflops_with_gather": job_flops * len(modes) / ((elapsed_ms / args.steps + float(gms.item())) * 1e-3) / 1e12}
 
     # --------------------------------------------------------- sampled parity of this launch config
     parity = None
@@ -368,14 +406,17 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "scaling": "strong" if nshard else "weak", "vs_baseline": None, "dtype": "f16",
             "data": "synthetic (seeded uniform[-1,1) inputs rounded to F16; C_in uniform F32/F16)",
             "config": {"workload": f"M=N=K={n} C+=A.B, F16 A/B row-major; one F32-acc and one F16-acc GEMM "
                                    f"per step" if len(modes) == 2 else f"M=N=K={n}, {modes[0]} acc",
                        "M": M, "N": N, "K": K, "modes": modes,
                        "kernel_config": args.config,
                        "l2": "inputs larger than L2 (A 128 MB + B 128 MB + C 256/128 MB per step > 126 MB)",
-                       "parallelism": "single GPU" if world == 1 else f"batch-one-per-GPU x{world} (no collective)"},
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"N-shard x{world}: A replicated, B/C column slabs" if nshard else
+                                       f"batch-one-per-GPU x{world} (no collective)"),
+                       "workload_kind": args.workload},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
                          "frac": achieved / peaks["tflops"], "traffic": traffic, "kernel": f"gemm {dom}-acc",
                          "peak_source": peaks["source"],
@@ -386,6 +427,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "parity": parity,
+            "allgather": gather,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -66,6 +66,12 @@ typedef struct {
   int config;       /* gemm_config_t; GEMM_CFG_AUTO picks from the shape              */
   int max_clusters; /* 0: one persistent cluster per resident slot; >0: cap the grid   */
   int group_m;      /* 0: default raster group height (tiles); >0: override            */
+  int l2_hints;     /* 0: default; 1: TMA L2 eviction hints on; -1: off                 */
+  int debug_flags;  /* 0 for real work.  DIAGNOSTIC ONLY (results are wrong): 1 = skip   */
+                    /* operand loads after the ring fills, 2 = skip C_in/C_out traffic   */
+  int promote_k;    /* K elements per TMEM accumulation chunk before the partial sum is  */
+                    /* added into F32 registers (RN): 0 = default 2048, -1 = never       */
+                    /* (one TMEM chain per tile), else a positive multiple of 64         */
 } gemm_options_t;
 
 /*

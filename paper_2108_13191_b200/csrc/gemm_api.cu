@@ -21,6 +21,8 @@ namespace {
 
 using namespace g16;
 
+constexpr int kDefaultL2Hints = 1;
+
 thread_local int t_last_cuda_error = 0;
 thread_local int t_last_launches = 0;
 
@@ -38,24 +40,32 @@ using Cfg5F16 = KCfg<1, 64, 8, true>;
 using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const GemmParams);
 
 struct ConfigDesc {
-  int cta_group, tile_n, stages, smem[2];
-  KernelFn fn[2];  // [acc_type]
+  int cta_group, tile_n, stages, threads;
+  int smem[2];      // [acc_type]
+  int c_box_cols[2];  // epilogue staging box width (elements)
+  int c_row_bytes[2]; // 128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B
+  KernelFn fn[2];
 };
 
 template <class C32, class C16>
 constexpr ConfigDesc make_desc() {
-  return ConfigDesc{C32::CG, C32::BN, C32::STAGES, {C32::SMEM_BYTES, C16::SMEM_BYTES},
+  return ConfigDesc{C32::CG, C32::BN, C32::STAGES, C32::THREADS,
+                    {C32::SMEM_BYTES, C16::SMEM_BYTES}, {C32::CW, C16::CW}, {C32::RB, C16::RB},
                     {&gemm_f16_sm100_kernel<C32>, &gemm_f16_sm100_kernel<C16>}};
 }
 
 const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
-    ConfigDesc{0, 0, 0, {0, 0}, {nullptr, nullptr}},
+    ConfigDesc{0, 0, 0, 0, {0, 0}, {0, 0}, {0, 0}, {nullptr, nullptr}},
     make_desc<Cfg1F32, Cfg1F16>(),
     make_desc<Cfg2F32, Cfg2F16>(),
     make_desc<Cfg3F32, Cfg3F16>(),
     make_desc<Cfg4F32, Cfg4F16>(),
     make_desc<Cfg5F32, Cfg5F16>(),
 };
+
+// K elements accumulated in TMEM before the partial sum is promoted to F32
+// registers (R4): 2048 keeps the truncation error near 2.4e-6.
+constexpr int kDefaultPromoteK = 2048;
 
 // ---------------------------------------------------------------- device cache
 constexpr int kMaxDevices = 64;
@@ -92,7 +102,7 @@ void init_device(int dev) {
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         lc.gridDim = dim3(2 * (d.sm_count / 2), 1, 1);
-        lc.blockDim = dim3(256, 1, 1);
+        lc.blockDim = dim3(cd.threads, 1, 1);
         lc.dynamicSmemBytes = cd.smem[a];
         lc.attrs = attr;
         lc.numAttrs = 1;
@@ -102,7 +112,7 @@ void init_device(int dev) {
         d.max_clusters[c][a] = n;
       } else {
         int per_sm = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cd.fn[a], 256, cd.smem[a]);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cd.fn[a], cd.threads, cd.smem[a]);
         if (e != cudaSuccess || per_sm <= 0) { d.status = GEMM_ERR_CUDA; d.cuda_error = e ? e : cudaErrorInvalidConfiguration; return; }
         d.max_clusters[c][a] = per_sm * d.sm_count;
       }
@@ -129,7 +139,8 @@ PFN_encodeTiled get_encode_fn() {
 
 // 2-D row-major tensor (rows x cols, ld elements), box = box_cols x box_rows, 128B swizzle.
 bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* ptr, int64_t rows,
-               int64_t cols, int64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapL2promotion l2) {
+               int64_t cols, int64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapL2promotion l2,
+               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   PFN_encodeTiled enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -137,7 +148,7 @@ bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void*
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   swz, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -207,11 +218,10 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const bool ok =
       encode_2d(&tm_a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, A, M, K, lda, 64, 128, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
       encode_2d(&tm_b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, B, K, N, ldb, 64, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
-      (acc_type == GEMM_ACC_F32
-           ? encode_2d(&tm_c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, M, N, ldc, 32, 32,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B)
-           : encode_2d(&tm_c, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, C, M, N, ldc, 64, 32,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B));
+      encode_2d(&tm_c, acc_type == GEMM_ACC_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                acc_type == GEMM_ACC_F32 ? 4 : 2, C, M, N, ldc, static_cast<uint32_t>(cd.c_box_cols[a]), 32,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                cd.c_row_bytes[a] == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return cuda_fail(cudaErrorInvalidValue);
 
   GemmParams p;
@@ -225,12 +235,20 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (tiles > 0x7fffffffLL) return GEMM_ERR_INVALID_VALUE;
   p.num_tiles = static_cast<int>(tiles);
   p.k_blocks = static_cast<int>(cdiv(K, 64));
+  const int promote = opts ? opts->promote_k : 0;
+  if (promote < -1 || (promote > 0 && promote % 64 != 0)) return GEMM_ERR_INVALID_VALUE;
+  p.kb_per_chunk = promote == -1 ? p.k_blocks : (promote == 0 ? kDefaultPromoteK : promote) / 64;
+  p.k_chunks = static_cast<int>(cdiv(p.k_blocks, p.kb_per_chunk));
   p.group_m = (opts && opts->group_m > 0) ? opts->group_m : 8;
   if (opts && opts->group_m < 0) return GEMM_ERR_INVALID_VALUE;
   const int64_t csize = acc_type == GEMM_ACC_F32 ? 4 : 2;
   p.c_ragged = (N * csize) % 16 != 0;
   p.c_ptr = C;
   p.ldc = ldc;
+  const int hints = opts ? opts->l2_hints : 0;
+  if (hints < -1 || hints > 1) return GEMM_ERR_INVALID_VALUE;
+  p.l2_hints = hints == 0 ? kDefaultL2Hints : (hints > 0 ? 1 : 0);
+  p.debug_flags = opts ? opts->debug_flags : 0;
 
   int clusters = di.max_clusters[cfg][a];
   if (opts && opts->max_clusters > 0) clusters = std::min(clusters, opts->max_clusters);
@@ -240,7 +258,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   cudaLaunchConfig_t lc = {};
   cudaLaunchAttribute attr[1];
   lc.gridDim = dim3(static_cast<unsigned>(clusters * cd.cta_group), 1, 1);
-  lc.blockDim = dim3(256, 1, 1);
+  lc.blockDim = dim3(static_cast<unsigned>(cd.threads), 1, 1);
   lc.dynamicSmemBytes = cd.smem[a];
   lc.stream = stream;
   if (cd.cta_group == 2) {

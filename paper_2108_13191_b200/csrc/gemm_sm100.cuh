@@ -8,17 +8,27 @@
 //  block tile tbm x tbn x tbk in smem (A3,A4)   CTA-pair tile (128*CG) x BN x 64, TMA-loaded
 //  padded smem leading dim (Sec 3.3)     128B hardware swizzle (TMA + UMMA descriptors)
 //  warp tiles + WMMA 16x16x16 (Sec 3.4)         one thread issues tcgen05.mma M=128*CG,N=BN,K=16
-//  C in registers, hoisted          accumulator in TMEM for the whole K loop
+//  C in registers, hoisted          accumulator in TMEM for a K chunk, promoted to
+//                                               F32 registers of the epilogue warps (see below)
 //  1-stage k-loop split (Sec 3.5)    STAGES-deep mbarrier ring (full/empty)
 //  __syncthreads around copies (Sec 3.6)        per-stage mbarriers + tcgen05.commit
 //  128-bit vector global->smem copies (3.7)     cp.async.bulk.tensor boxes of 8-16 KB
 //  one thread block per C tile (Sec 3.9)        persistent clusters, grouped raster schedule
-//  C stored once per warp tile      epilogue warps: TMEM -> regs (+C_in) -> smem
-//                                               -> TMA store, overlapped with the next tile's
-//                                               mainloop through a double-buffered TMEM acc
+//  C stored once per warp tile      C_in added once in F32; smem -> TMA store,
+//                                               overlapped with the next chunk's MMAs
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (pair leader only),
-// w2 TMEM allocator, w3 idle, w4..w7 epilogue (warp w reads TMEM lanes 32*(w%4)..).
+// Accumulation (R4): the tensor cores' F32 accumulator truncates on
+// every K=16 step, so a single TMEM chain's relative error grows ~1.2e-6 per
+// 1024 of K (measured; bitwise the same as cuBLAS) and crosses BASELINE's 1e-5
+// bound near K = 8400.  The K loop is therefore cut into chunks of
+// `kb_per_chunk` k-blocks: each chunk accumulates in a fresh TMEM buffer
+// (double-buffered, so the MMA never waits for the drain), and the epilogue
+// warps add the chunk into F32 registers with round-to-nearest adds.  The
+// error then scales with the chunk length, not with K.
+//
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer (pair leader only),
+// w2 TMEM allocator, w3 idle, w4..w11 epilogue.  Epilogue warp e = w-4 reads
+// TMEM lanes 32*(w%4).. (hardware quadrant rule) and columns [e/4 * BN/2, +BN/2).
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -30,15 +40,22 @@ struct GemmParams {
   int M, N, K;
   int tiles_m, tiles_n, num_tiles;  // tiles of (128*CG) x BN
   int k_blocks;                     // ceil(K / 64)
+  int kb_per_chunk;                 // k-blocks accumulated in TMEM before promotion to registers
+  int k_chunks;                     // ceil(k_blocks / kb_per_chunk)
   int group_m;                      // raster group height in tiles
   int c_ragged;                     // N * sizeof(C) % 16 != 0: TMA stores would write a
                                     // whole 16-byte granule past column N-1, so the chunk
                                     // holding column N-1 is stored element-wise instead
   void* c_ptr;                      // C base (used only by that ragged-N store path)
   long long ldc;                    // C leading dimension in elements
+  int debug_flags;                  // DIAGNOSTIC ONLY (wrong results): 1 = no operand TMA after
+                                    // the ring is filled once per tile, 2 = no C_in/C_out traffic
+  int l2_hints;                     // 1: TMA loads/stores carry L2 eviction-priority hints
+                                    // (A evict_last: re-read by the next wave of tiles;
+                                    //  C evict_first: streamed once)
 };
 
-template <int CG_, int BN_, int STAGES_, bool OUT_F16_>
+template <int CG_, int BN_, int STAGES_, bool OUT_F16_, int EPI_SLOTS_ = 1>
 struct KCfg {
   static constexpr int CG = CG_;            // CTAs per MMA (cta_group)
   static constexpr int BN = BN_;            // UMMA N (tile columns)
@@ -49,28 +66,31 @@ struct KCfg {
   static constexpr int UMMA_K = 16;
   static constexpr int BN_CTA = BN / CG;    // B columns staged per CTA
   static_assert(BN_CTA % 64 == 0, "B is staged in 64-column (128 B) swizzle atoms");
-  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
+  static_assert(BN % 64 == 0 && BN <= 256, "UMMA N");
   static constexpr int A_BYTES = BM * BK * 2;         // 16 KB
   static constexpr int B_ATOM_BYTES = 64 * BK * 2;    // 64 cols x 64 k = 8 KB
   static constexpr int B_BYTES = BN_CTA * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int ACC_COLS = BN;                 // one accumulator buffer
-  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
-                                   : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int CW = OUT_F16 ? 64 : 32;        // epilogue chunk width (128 B of C)
-  static constexpr int NCHUNK = BN / CW;
-  static constexpr int EPI_WARPS = 4;
-  static constexpr int EPI_SLOTS = 2;
-  static constexpr int EPI_BUF = 32 * 128;            // 32 rows x 128 B
+  static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int EPI_WARPS = 8;
+  static constexpr int CPW = BN / 2;                  // accumulator columns per epilogue warp
+  static constexpr int ESIZE = OUT_F16 ? 2 : 4;
+  static constexpr int CW = (128 / ESIZE < CPW) ? 128 / ESIZE : CPW;   // output chunk columns
+  static constexpr int RB = CW * ESIZE;               // staging row bytes: 128 or 64
+  static_assert(RB == 128 || RB == 64, "staging rows are one 128B or 64B swizzle span");
+  static constexpr int NOUT = CPW / CW;               // output chunks per warp per tile
+  static constexpr int EPI_SLOTS = EPI_SLOTS_;
+  static constexpr int EPI_BUF = 32 * 128;            // 32 rows x up to 128 B
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = STAGES * A_BYTES;
   static constexpr int OFF_E = STAGES * STAGE_BYTES;
   static constexpr int OFF_BAR = OFF_E + EPI_WARPS * EPI_SLOTS * EPI_BUF;
-  // barriers: full[S], empty[S], acc_full[2], acc_empty[2], epi[4][2], tmem slot
+  // barriers: full[S], empty[S], acc_full[2], acc_empty[2], epi[8][slots], tmem slot
   static constexpr int NBAR = 2 * STAGES + 4 + EPI_WARPS * EPI_SLOTS;
   static constexpr int SMEM_BYTES = 1024 + OFF_BAR + NBAR * 8 + 16;
   static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of dynamic shared memory");
-  static constexpr int THREADS = 256;
+  static constexpr int THREADS = 384;                 // 12 warps x <= 168 registers fit 64K
 };
 
 // UMMA shared-memory descriptor, SWIZZLE_128B layout (sm_100 "version 1").
@@ -109,8 +129,15 @@ __device__ __forceinline__ void tile_coords(int tile, const GemmParams& p, int& 
   tn = local / gs;
 }
 
+// Byte offset of 16-byte unit j of row r in a TMA-swizzled staging box whose
+// rows are RB bytes (128B swizzle: j ^ r%8; 64B swizzle: j ^ (r/2)%4).
+template <int RB>
+__device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t j) {
+  return r * RB + ((j ^ (((r * RB) >> 7) & (RB / 16 - 1))) << 4);
+}
+
 template <class Cfg>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                       const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_c,
@@ -164,6 +191,8 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     // ===================== TMA producer =====================
     if (lane == 0) {
       const uint32_t full_leader = (CG == 2) ? mapa_shared(full_bar, 0) : full_bar;
+      const uint64_t pol_a = p.l2_hints ? policy_evict_last() : policy_evict_normal();
+      const uint64_t pol_b = policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
@@ -173,20 +202,25 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         const int b_col = tn * BN + static_cast<int>(rank) * Cfg::BN_CTA;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(empty_bar + 8 * stage, phase ^ 1u);
+          if ((p.debug_flags & 1) && kb >= STAGES) {
+            if (rank == 0) mbar_arrive(full_bar + 8 * stage);
+            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            continue;
+          }
           if (rank == 0) mbar_arrive_expect_tx(full_bar + 8 * stage, Cfg::STAGE_BYTES * CG);
           const uint32_t fb = full_leader + 8 * stage;
           const uint32_t a_dst = sA + stage * Cfg::A_BYTES;
           const uint32_t b_dst = sB + stage * Cfg::B_BYTES;
           if constexpr (CG == 2) {
-            tma_load_2d_pair(a_dst, &tm_a, kb * BK, a_row, fb);
+            tma_load_2d_pair_hint(a_dst, &tm_a, kb * BK, a_row, fb, pol_a);
 #pragma unroll
             for (int h = 0; h < Cfg::BN_CTA / 64; ++h)
-              tma_load_2d_pair(b_dst + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h, kb * BK, fb);
+              tma_load_2d_pair_hint(b_dst + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h, kb * BK, fb, pol_b);
           } else {
-            tma_load_2d(a_dst, &tm_a, kb * BK, a_row, fb);
+            tma_load_2d_hint(a_dst, &tm_a, kb * BK, a_row, fb, pol_a);
 #pragma unroll
             for (int h = 0; h < Cfg::BN_CTA / 64; ++h)
-              tma_load_2d(b_dst + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h, kb * BK, fb);
+              tma_load_2d_hint(b_dst + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h, kb * BK, fb, pol_b);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
@@ -201,98 +235,123 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
-        mbar_wait_cluster(acce_bar + 8 * acc, acc_phase ^ 1u);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
-          mbar_wait(full_bar + 8 * stage, phase);
+        for (int ch = 0; ch < p.k_chunks; ++ch) {
+          mbar_wait_cluster(acce_bar + 8 * acc, acc_phase ^ 1u);
           tc_fence_after();
-          const uint32_t a_s = sA + stage * Cfg::A_BYTES;
-          const uint32_t b_s = sB + stage * Cfg::B_BYTES;
+          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
+          const int kb0 = ch * p.kb_per_chunk;
+          const int kb1 = min(kb0 + p.kb_per_chunk, p.k_blocks);
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(full_bar + 8 * stage, phase);
+            tc_fence_after();
+            const uint32_t a_s = sA + stage * Cfg::A_BYTES;
+            const uint32_t b_s = sB + stage * Cfg::B_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / Cfg::UMMA_K; ++k) {
-            // A (K-major): advance 16 elements = 32 B inside the 128B swizzle row.
-            const uint64_t adesc = desc_sw128(a_s + 32 * k, 16, 1024);
-            // B (MN-major): advance 16 k-rows = 2 swizzle atoms of 8 rows x 128 B;
-            // 64-column groups are B_ATOM_BYTES apart (LBO), 8-row groups 1 KB (SBO).
-            const uint64_t bdesc = desc_sw128(b_s + 2048 * k, Cfg::B_ATOM_BYTES, 1024);
-            umma_f16<CG>(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < BK / Cfg::UMMA_K; ++k) {
+              // A (K-major): advance 16 elements = 32 B inside the 128B swizzle row.
+              const uint64_t adesc = desc_sw128(a_s + 32 * k, 16, 1024);
+              // B (MN-major): advance 16 k-rows = 2 swizzle atoms of 8 rows x 128 B;
+              // 64-column groups are B_ATOM_BYTES apart (LBO), 8-row groups 1 KB (SBO).
+              const uint64_t bdesc = desc_sw128(b_s + 2048 * k, Cfg::B_ATOM_BYTES, 1024);
+              umma_f16<CG>(d_tmem, adesc, bdesc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
+            if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, 0x3);
+            else umma_commit(empty_bar + 8 * stage);
+            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
           }
-          if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, 0x3);
-          else umma_commit(empty_bar + 8 * stage);
-          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, 0x3);
+          else umma_commit(accf_bar + 8 * acc);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
         }
-        if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, 0x3);
-        else umma_commit(accf_bar + 8 * acc);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
       }
     }
   } else if (warp >= 4) {
     // ===================== epilogue warps =====================
-    const uint32_t ew = warp - 4;          // == warp % 4: TMEM lane quadrant
-    const uint32_t q = warp & 3;
+    const uint32_t ew = warp - 4;                 // 0..7
+    const uint32_t q = warp & 3;                  // TMEM lane quadrant (hardware rule: warp % 4)
+    const uint32_t hcol = (ew >> 2) * Cfg::CPW;   // first accumulator column of this warp
     const uint32_t ebuf0 = sE + ew * Cfg::EPI_SLOTS * Cfg::EPI_BUF;
     const uint32_t ebar0 = epi_bar + 8 * Cfg::EPI_SLOTS * ew;
     const uint32_t acce_leader = (CG == 2) ? mapa_shared(acce_bar, 0) : acce_bar;
+    const uint64_t pol_c = p.l2_hints ? policy_evict_first() : policy_evict_normal();
+    const bool no_c = (p.debug_flags & 2) != 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint32_t chunk_ctr = 0;
+    uint32_t out_ctr = 0;
     uint32_t slot_phase = 0;  // bit s = parity to wait for on slot s
+    float racc[Cfg::CPW];
     for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
       int tm, tn;
       tile_coords(tile, p, tm, tn);
       const int row0 = tm * BM * CG + static_cast<int>(rank) * BM + static_cast<int>(q) * 32;
-      const int col0 = tn * BN;
-      if (lane == 0) {
+      const int col0 = tn * BN + static_cast<int>(hcol);
+      if (lane == 0 && !no_c) {
 #pragma unroll 1
-        for (int c = 0; c < Cfg::NCHUNK; ++c) tma_prefetch_l2_2d(&tm_c, col0 + c * Cfg::CW, row0);
+        for (int c = 0; c < Cfg::NOUT; ++c) tma_prefetch_l2_2d(&tm_c, col0 + c * Cfg::CW, row0);
       }
-      mbar_wait(accf_bar + 8 * acc, acc_phase);
-      tc_fence_after();
-      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
+      // ---- promote each K chunk's TMEM partial sum into F32 registers (RN adds)
+      const uint32_t t_lane = tmem_base + ((q * 32u) << 16) + hcol;
 #pragma unroll 1
-      for (int c = 0; c < Cfg::NCHUNK; ++c) {
-        const uint32_t slot = chunk_ctr & 1u;
-        const uint32_t sbuf = ebuf0 + slot * Cfg::EPI_BUF;
-        const uint32_t sbar = ebar0 + 8 * slot;
-        if (lane == 0) {
-          bulk_wait_group_read<1>();   // the store that last used this slot has read it
-          mbar_arrive_expect_tx(sbar, Cfg::EPI_BUF);
-          tma_load_2d(sbuf, &tm_c, col0 + c * Cfg::CW, row0, sbar);
-        }
-        __syncwarp();
-        uint32_t v0[32];
-        uint32_t v1[32];
-        tmem_ld_32x32b_x32(t_row + c * Cfg::CW, v0);
-        if constexpr (Cfg::OUT_F16) tmem_ld_32x32b_x32(t_row + c * Cfg::CW + 32, v1);
-        tmem_wait_ld();
-        if (c == Cfg::NCHUNK - 1) {
-          // accumulator buffer fully read into registers: hand it back to the MMA warp
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if constexpr (CG == 2) mbar_arrive_cluster(acce_leader + 8 * acc);
-            else mbar_arrive(acce_bar + 8 * acc);
+      for (int ch = 0; ch < p.k_chunks; ++ch) {
+        mbar_wait(accf_bar + 8 * acc, acc_phase);
+        tc_fence_after();
+        const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
+#pragma unroll
+        for (int c = 0; c < Cfg::CPW / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + 32 * c, v);
+          tmem_wait_ld();
+          if (ch == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) racc[32 * c + j] = __uint_as_float(v[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) racc[32 * c + j] = __fadd_rn(racc[32 * c + j], __uint_as_float(v[j]));
           }
         }
+        // chunk fully read: hand the TMEM buffer back to the MMA warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(acce_leader + 8 * acc);
+          else mbar_arrive(acce_bar + 8 * acc);
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+      }
+      // ---- C_out = C_in + acc (F32 add, one rounding to the output type), TMA store
+      const int grow = row0 + static_cast<int>(lane);
+#pragma unroll
+      for (int c = 0; c < Cfg::NOUT; ++c) {
+        const uint32_t slot = (Cfg::EPI_SLOTS == 1) ? 0u : (out_ctr & 1u);
+        const uint32_t sbuf = ebuf0 + slot * Cfg::EPI_BUF;
+        const uint32_t sbar = ebar0 + 8 * slot;
+        const int ccol = col0 + c * Cfg::CW;
+        const bool manual = p.c_ragged && (ccol + Cfg::CW > p.N);
+        if (lane == 0) {
+          if constexpr (Cfg::EPI_SLOTS == 1) bulk_wait_group_read<0>();
+          else bulk_wait_group_read<1>();   // the store that last used this slot has read it
+          if (!no_c) {
+            mbar_arrive_expect_tx(sbar, 32 * Cfg::RB);
+            tma_load_2d_hint(sbuf, &tm_c, ccol, row0, sbar, pol_c);
+          } else {
+            mbar_arrive(sbar);
+          }
+        }
+        __syncwarp();
         mbar_wait(sbar, (slot_phase >> slot) & 1u);
         slot_phase ^= (1u << slot);
-        // Row `lane` of the 32x128B box; 16-byte unit j sits at j ^ (row % 8) (128B swizzle).
-        const uint32_t row_addr = sbuf + lane * 128u;
-        const bool manual = p.c_ragged && (col0 + (c + 1) * Cfg::CW > p.N);
-        const int grow = row0 + static_cast<int>(lane);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t addr = row_addr + ((static_cast<uint32_t>(j) ^ (lane & 7u)) << 4);
+        for (int j = 0; j < Cfg::RB / 16; ++j) {
+          const uint32_t addr = sbuf + swz<Cfg::RB>(lane, static_cast<uint32_t>(j));
+          const float* a = &racc[c * Cfg::CW + j * (16 / Cfg::ESIZE)];
           if constexpr (!Cfg::OUT_F16) {
             const float4 ci = lds128(addr);
-            const float o0 = ci.x + __uint_as_float(v0[4 * j + 0]), o1 = ci.y + __uint_as_float(v0[4 * j + 1]);
-            const float o2 = ci.z + __uint_as_float(v0[4 * j + 2]), o3 = ci.w + __uint_as_float(v0[4 * j + 3]);
+            const float o0 = ci.x + a[0], o1 = ci.y + a[1], o2 = ci.z + a[2], o3 = ci.w + a[3];
             if (!manual) {
               sts128(addr, o0, o1, o2, o3);
             } else if (grow < p.M) {
               float* dst = static_cast<float*>(p.c_ptr) + static_cast<long long>(grow) * p.ldc;
-              const int cb = col0 + c * Cfg::CW + 4 * j;
+              const int cb = ccol + 4 * j;
               const float o[4] = {o0, o1, o2, o3};
 #pragma unroll
               for (int e = 0; e < 4; ++e)
@@ -300,18 +359,17 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
             }
           } else {
             const uint4 ci = lds128u(addr);
-            const uint32_t* src = (j < 4) ? &v0[8 * j] : &v1[8 * (j - 4)];
             const float2 c0 = f16x2_to_f32(ci.x), c1 = f16x2_to_f32(ci.y);
             const float2 c2 = f16x2_to_f32(ci.z), c3 = f16x2_to_f32(ci.w);
-            const uint32_t o0 = cvt_f16x2_rn(c0.x + __uint_as_float(src[0]), c0.y + __uint_as_float(src[1]));
-            const uint32_t o1 = cvt_f16x2_rn(c1.x + __uint_as_float(src[2]), c1.y + __uint_as_float(src[3]));
-            const uint32_t o2 = cvt_f16x2_rn(c2.x + __uint_as_float(src[4]), c2.y + __uint_as_float(src[5]));
-            const uint32_t o3 = cvt_f16x2_rn(c3.x + __uint_as_float(src[6]), c3.y + __uint_as_float(src[7]));
+            const uint32_t o0 = cvt_f16x2_rn(c0.x + a[0], c0.y + a[1]);
+            const uint32_t o1 = cvt_f16x2_rn(c1.x + a[2], c1.y + a[3]);
+            const uint32_t o2 = cvt_f16x2_rn(c2.x + a[4], c2.y + a[5]);
+            const uint32_t o3 = cvt_f16x2_rn(c3.x + a[6], c3.y + a[7]);
             if (!manual) {
               sts128u(addr, o0, o1, o2, o3);
             } else if (grow < p.M) {
               uint16_t* dst = static_cast<uint16_t*>(p.c_ptr) + static_cast<long long>(grow) * p.ldc;
-              const int cb = col0 + c * Cfg::CW + 8 * j;
+              const int cb = ccol + 8 * j;
               const uint32_t o[4] = {o0, o1, o2, o3};
 #pragma unroll
               for (int e = 0; e < 8; ++e)
@@ -319,19 +377,18 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
             }
           }
         }
-        if (!manual) {
+        if (!manual && !no_c) {
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tm_c, col0 + c * Cfg::CW, row0, sbuf);
+            tma_store_2d_hint(&tm_c, ccol, row0, sbuf, pol_c);
             bulk_commit_group();
           }
         } else {
           __syncwarp();
         }
-        ++chunk_ctr;
+        ++out_ctr;
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
     if (lane == 0) bulk_wait_group<0>();
   }

@@ -198,3 +198,33 @@ def test_errors_are_reported(g):
     C0 = C.clone()
     g.gemm_f16(A[:, :0], B[:0, :], C)
     assert g.last_launches() == 0 and torch.equal(C, C0)
+
+
+@pytest.mark.parametrize("promote_k", [64, 128, 512, 2048, -1])
+@pytest.mark.parametrize("cfg", ["pair_256x256", "solo_128x64"])
+def test_promotion_chunk_lengths(g, promote_k, cfg):
+    """K chunks of every length (incl. one chunk per k-block and a ragged last
+    chunk) give oracle parity; -1 = one TMEM chain per tile."""
+    M, N, K = 600, 712, 1000
+    A, B, C, gA, gB, gC = device_problem(M, N, K, "f32", seed=12)
+    _run(g, gA, gB, gC, config=cfg, promote_k=promote_k)
+    ex, _ = oracle_full(A, B, C)
+    check(gC.result(), ex, A, B, "f32", K, f"promote_k={promote_k}")
+
+
+def test_promotion_bounds_long_k_error(g):
+    """DESIGN.md R4: a single TMEM chain truncates, so its error grows with K and
+    fails the 1e-5 bound at K=16384; chunked promotion (default) keeps it small."""
+    import torch
+    M, N, K = 256, 512, 16384
+    A, B, C = synth.problem(M, N, K, "f32", seed=2)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    ex, _ = oracle.gemm(A, B, C)
+    rel = {}
+    for pk in (0, -1):
+        dC = torch.from_numpy(C.copy()).cuda()
+        g.gemm_f16(dA, dB, dC, promote_k=pk)
+        torch.cuda.synchronize()
+        rel[pk] = stats(dC.cpu().numpy(), ex)["rel_fro"]
+    print(f"K=16384 rel_fro: promoted {rel[0]:.3e}, single chain {rel[-1]:.3e}")
+    assert rel[0] <= 5e-6 < rel[-1]
