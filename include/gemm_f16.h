@@ -59,7 +59,8 @@ typedef enum {
   GEMM_CFG_SOLO_128x256 = 3, /* cta_group::1, UMMA 128x256x16               */
   GEMM_CFG_SOLO_128x128 = 4, /* cta_group::1, UMMA 128x128x16               */
   GEMM_CFG_SOLO_128x64 = 5,  /* cta_group::1, UMMA 128x64x16                */
-  GEMM_CFG_COUNT = 6
+  GEMM_CFG_PAIR_256x256_S5 = 6, /* as PAIR_256x256 with 5 stages and a double-buffered epilogue */
+  GEMM_CFG_COUNT = 7
 } gemm_config_t;
 
 typedef struct {
@@ -72,6 +73,8 @@ typedef struct {
   int promote_k;    /* K elements per TMEM accumulation chunk before the partial sum is  */
                     /* added into F32 registers (RN): 0 = default 2048, -1 = never       */
                     /* (one TMEM chain per tile), else a positive multiple of 64         */
+  int epi_pace;     /* 0: default; 1: pace each tile's C traffic over half a K-chunk      */
+                    /* interval; -1: store as fast as possible                           */
 } gemm_options_t;
 
 /*

@@ -22,6 +22,7 @@ namespace {
 using namespace g16;
 
 constexpr int kDefaultL2Hints = 1;
+constexpr int kDefaultEpiPace = 1;
 
 thread_local int t_last_cuda_error = 0;
 thread_local int t_last_launches = 0;
@@ -36,6 +37,8 @@ using Cfg4F32 = KCfg<1, 128, 6, false>;
 using Cfg4F16 = KCfg<1, 128, 6, true>;
 using Cfg5F32 = KCfg<1, 64, 8, false>;
 using Cfg5F16 = KCfg<1, 64, 8, true>;
+using Cfg6F32 = KCfg<2, 256, 5, false, 2>;
+using Cfg6F16 = KCfg<2, 256, 5, true, 2>;
 
 using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const GemmParams);
 
@@ -61,6 +64,7 @@ const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
     make_desc<Cfg3F32, Cfg3F16>(),
     make_desc<Cfg4F32, Cfg4F16>(),
     make_desc<Cfg5F32, Cfg5F16>(),
+    make_desc<Cfg6F32, Cfg6F16>(),
 };
 
 // K elements accumulated in TMEM before the partial sum is promoted to F32
@@ -249,6 +253,9 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (hints < -1 || hints > 1) return GEMM_ERR_INVALID_VALUE;
   p.l2_hints = hints == 0 ? kDefaultL2Hints : (hints > 0 ? 1 : 0);
   p.debug_flags = opts ? opts->debug_flags : 0;
+  const int pace = opts ? opts->epi_pace : 0;
+  if (pace < -1 || pace > 1) return GEMM_ERR_INVALID_VALUE;
+  p.epi_pace = pace == 0 ? kDefaultEpiPace : (pace > 0 ? 1 : 0);
 
   int clusters = di.max_clusters[cfg][a];
   if (opts && opts->max_clusters > 0) clusters = std::min(clusters, opts->max_clusters);
