@@ -419,6 +419,8 @@ def main():
                        "workload_kind": args.workload},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
                          "frac": achieved / peaks["tflops"], "traffic": traffic, "kernel": f"gemm {dom}-acc",
+                         "algorithmic_flops_per_launch": flops,
+                         "algorithmic_bytes_per_launch": 2 * (M * K + K * nr) + 2 * M * nr * (4 if dom == "f32" else 2),
                          "peak_source": peaks["source"],
                          "frac_of_nominal_2250": achieved / NOMINAL_F16_DENSE_TFLOPS},
             "modes": mode_stats,
