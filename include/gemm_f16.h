@@ -65,7 +65,9 @@ typedef enum {
 
 typedef struct {
   int config;       /* gemm_config_t; GEMM_CFG_AUTO picks from the shape              */
-  int max_clusters; /* 0: one persistent cluster per resident slot; >0: cap the grid   */
+  int max_clusters; /* 0: one persistent cluster per resident slot; >0: exactly this   */
+                    /* many clusters (capped at the tile count; more than the resident */
+                    /* slots gives a non-persistent launch)                            */
   int group_m;      /* 0: default raster group height (tiles); >0: override            */
   int l2_hints;     /* 0: default; 1: TMA L2 eviction hints on; -1: off                 */
   int debug_flags;  /* 0 for real work.  DIAGNOSTIC ONLY (results are wrong): 1 = skip   */
@@ -75,6 +77,8 @@ typedef struct {
                     /* (one TMEM chain per tile), else a positive multiple of 64         */
   int epi_pace;     /* 0: default; 1: pace each tile's C traffic over half a K-chunk      */
                     /* interval; -1: store as fast as possible                           */
+  int ring_stages;  /* 0: all stages of the config; 1..stages: use a shallower smem ring   */
+  int acc_bufs;     /* 0 or 2: double-buffered TMEM accumulator; 1: single (no overlap)   */
 } gemm_options_t;
 
 /*

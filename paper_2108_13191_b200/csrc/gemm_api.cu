@@ -158,12 +158,16 @@ bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void*
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Shape -> configuration (the paper's per-size "best performing version",
+// P:903-905, as a fixed table so results stay deterministic).  Measured on B200
+// (profiles/r01/cfgsweep.md): the 2-CTA 256x256 pair tile wins at every
+// BASELINE shape from 2048^3 up, including the BERT shapes and tails, even when
+// it fills less than one wave -- smaller tiles lose more to per-FLOP operand
+// traffic than they gain in parallelism.  Only a short M (<= 128 rows) wastes
+// enough of a 256-row pair tile to prefer a 1-CTA tile.
 int pick_config(int64_t M, int64_t N, int sm_count) {
-  const int64_t pair_slots = sm_count / 2;
-  if (cdiv(M, 256) * cdiv(N, 256) >= pair_slots) return GEMM_CFG_PAIR_256x256;
-  if (cdiv(M, 256) * cdiv(N, 128) >= pair_slots) return GEMM_CFG_PAIR_256x128;
-  if (cdiv(M, 128) * cdiv(N, 128) >= sm_count) return GEMM_CFG_SOLO_128x128;
-  return GEMM_CFG_SOLO_128x64;
+  if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
+  return GEMM_CFG_PAIR_256x256;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -256,9 +260,17 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const int pace = opts ? opts->epi_pace : 0;
   if (pace < -1 || pace > 1) return GEMM_ERR_INVALID_VALUE;
   p.epi_pace = pace == 0 ? kDefaultEpiPace : (pace > 0 ? 1 : 0);
+  const int rs = opts ? opts->ring_stages : 0;
+  if (rs < 0 || rs > cd.stages) return GEMM_ERR_INVALID_VALUE;
+  p.ring_stages = rs == 0 ? cd.stages : rs;
+  const int ab = opts ? opts->acc_bufs : 0;
+  if (ab < 0 || ab > 2) return GEMM_ERR_INVALID_VALUE;
+  p.acc_bufs = ab == 0 ? 2 : ab;
 
+  // persistent grid: one cluster per resident slot; an explicit max_clusters may
+  // also exceed the resident slots (a non-persistent launch, for ablation)
   int clusters = di.max_clusters[cfg][a];
-  if (opts && opts->max_clusters > 0) clusters = std::min(clusters, opts->max_clusters);
+  if (opts && opts->max_clusters > 0) clusters = opts->max_clusters;
   if (opts && opts->max_clusters < 0) return GEMM_ERR_INVALID_VALUE;
   clusters = static_cast<int>(std::min<int64_t>(clusters, tiles));
 

@@ -53,6 +53,8 @@ struct GemmParams {
   long long ldc;                    // C leading dimension in elements
   int debug_flags;                  // DIAGNOSTIC ONLY (wrong results): 1 = no operand TMA after
                                     // the ring is filled once per tile, 2 = no C_in/C_out traffic
+  int ring_stages;                  // smem ring depth in use (1..STAGES; ablation of Sec 3.5)
+  int acc_bufs;                     // TMEM accumulator buffers in use (2 = epilogue overlaps MMA)
   int epi_pace;                     // 1: spread each tile's C_in/C_out traffic over half a K-chunk
                                     // interval instead of a burst synchronised across all SMs
   int l2_hints;                     // 1: TMA loads/stores carry L2 eviction-priority hints
@@ -208,9 +210,9 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         const int b_col = tn * BN + static_cast<int>(rank) * Cfg::BN_CTA;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(empty_bar + 8 * stage, phase ^ 1u);
-          if ((p.debug_flags & 1) && kb >= STAGES) {
+          if ((p.debug_flags & 1) && kb >= p.ring_stages) {
             if (rank == 0) mbar_arrive(full_bar + 8 * stage);
-            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
             continue;
           }
           if (rank == 0) mbar_arrive_expect_tx(full_bar + 8 * stage, Cfg::STAGE_BYTES * CG);
@@ -228,7 +230,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
             for (int h = 0; h < Cfg::BN_CTA / 64; ++h)
               tma_load_2d_hint(b_dst + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h, kb * BK, fb, pol_b);
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
         }
       }
     }
@@ -263,11 +265,11 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
             }
             if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, 0x3);
             else umma_commit(empty_bar + 8 * stage);
-            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
           }
           if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, 0x3);
           else umma_commit(accf_bar + 8 * acc);
-          if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+          if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1u; }
         }
       }
     }
@@ -331,7 +333,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           if constexpr (CG == 2) mbar_arrive_cluster(acce_leader + 8 * acc);
           else mbar_arrive(acce_bar + 8 * acc);
         }
-        if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+        if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1u; }
       }
       // ---- C_out = C_in + acc (F32 add, one rounding to the output type), TMA store.
       // Paced: output chunk c starts no earlier than c * chunk_ns / (2 * NOUT) after

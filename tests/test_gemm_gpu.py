@@ -228,3 +228,20 @@ def test_promotion_bounds_long_k_error(g):
         rel[pk] = stats(dC.cpu().numpy(), ex)["rel_fro"]
     print(f"K=16384 rel_fro: promoted {rel[0]:.3e}, single chain {rel[-1]:.3e}")
     assert rel[0] <= 5e-6 < rel[-1]
+
+
+@pytest.mark.parametrize("kw", [
+    {"ring_stages": 1}, {"ring_stages": 2}, {"acc_bufs": 1}, {"acc_bufs": 1, "ring_stages": 1},
+    {"group_m": 1}, {"group_m": 3}, {"l2_hints": -1}, {"epi_pace": -1}, {"max_clusters": 1000},
+    {"config": "pair_256x256_s5"}, {"config": "solo_128x256", "ring_stages": 1, "acc_bufs": 1},
+])
+def test_ablation_knobs_keep_parity(g, kw):
+    """Every ablation switch (used by tools/ablation.py) is a scheduling choice only:
+    results stay within the bar (and a 1-deep ring stresses the phase logic)."""
+    M, N, K = 777, 1040, 1216
+    for acc in ("f32", "f16"):
+        A, B, C, gA, gB, gC = device_problem(M, N, K, acc, seed=13)
+        _run(g, gA, gB, gC, **kw)
+        ex, _ = oracle_full(A, B, C)
+        check(gC.result(), ex, A, B, acc, K, f"{kw} {acc}")
+        assert gC.guard_intact()
