@@ -59,8 +59,9 @@ typedef enum {
   GEMM_CFG_SOLO_128x256 = 3, /* cta_group::1, UMMA 128x256x16               */
   GEMM_CFG_SOLO_128x128 = 4, /* cta_group::1, UMMA 128x128x16               */
   GEMM_CFG_SOLO_128x64 = 5,  /* cta_group::1, UMMA 128x64x16                */
-  GEMM_CFG_PAIR_256x256_S5 = 6, /* as PAIR_256x256 with 5 stages and a double-buffered epilogue */
-  GEMM_CFG_COUNT = 7
+  GEMM_CFG_PAIR_256x256_S5 = 6, /* as PAIR_256x256, 5 stages, 2 epilogue staging slots per warp */
+  GEMM_CFG_PAIR_256x256_S4 = 7, /* as PAIR_256x256, 4 stages, 3 epilogue staging slots per warp */
+  GEMM_CFG_COUNT = 8
 } gemm_config_t;
 
 typedef struct {
@@ -75,10 +76,12 @@ typedef struct {
   int promote_k;    /* K elements per TMEM accumulation chunk before the partial sum is  */
                     /* added into F32 registers (RN): 0 = default 2048, -1 = never       */
                     /* (one TMEM chain per tile), else a positive multiple of 64         */
-  int epi_pace;     /* 0: default; 1: pace each tile's C traffic over half a K-chunk      */
-                    /* interval; -1: store as fast as possible                           */
+  int epi_pace;     /* 0: default (off); 1: pace each tile's C traffic over half a K-chunk */
+                    /* interval; -1: off                                                  */
   int ring_stages;  /* 0: all stages of the config; 1..stages: use a shallower smem ring   */
   int acc_bufs;     /* 0 or 2: double-buffered TMEM accumulator; 1: single (no overlap)   */
+  void* trace;      /* DIAGNOSTIC ONLY, normally NULL: device buffer of 512 uint64 that   */
+                    /* receives per-tile globaltimer stamps of CTA 0                      */
 } gemm_options_t;
 
 /*

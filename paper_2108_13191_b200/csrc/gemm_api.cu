@@ -22,7 +22,7 @@ namespace {
 using namespace g16;
 
 constexpr int kDefaultL2Hints = 1;
-constexpr int kDefaultEpiPace = 1;
+constexpr int kDefaultEpiPace = 0;
 
 thread_local int t_last_cuda_error = 0;
 thread_local int t_last_launches = 0;
@@ -39,6 +39,8 @@ using Cfg5F32 = KCfg<1, 64, 8, false>;
 using Cfg5F16 = KCfg<1, 64, 8, true>;
 using Cfg6F32 = KCfg<2, 256, 5, false, 2>;
 using Cfg6F16 = KCfg<2, 256, 5, true, 2>;
+using Cfg7F32 = KCfg<2, 256, 4, false, 3>;
+using Cfg7F16 = KCfg<2, 256, 4, true, 3>;
 
 using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const GemmParams);
 
@@ -65,6 +67,7 @@ const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
     make_desc<Cfg4F32, Cfg4F16>(),
     make_desc<Cfg5F32, Cfg5F16>(),
     make_desc<Cfg6F32, Cfg6F16>(),
+    make_desc<Cfg7F32, Cfg7F16>(),
 };
 
 // K elements accumulated in TMEM before the partial sum is promoted to F32
@@ -160,13 +163,16 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Shape -> configuration (the paper's per-size "best performing version",
 // P:903-905, as a fixed table so results stay deterministic).  Measured on B200
-// (profiles/r01/cfgsweep.md): the 2-CTA 256x256 pair tile wins at every
-// BASELINE shape from 2048^3 up, including the BERT shapes and tails, even when
-// it fills less than one wave -- smaller tiles lose more to per-FLOP operand
-// traffic than they gain in parallelism.  Only a short M (<= 128 rows) wastes
-// enough of a 256-row pair tile to prefer a 1-CTA tile.
-int pick_config(int64_t M, int64_t N, int sm_count) {
+// (profiles/r01/cfgsweep.md, profiles/r01/epilogue_slots.md): the 2-CTA 256x256
+// pair tile wins at every BASELINE shape from 2048^3 up, including the BERT
+// shapes and tails, even below one wave -- smaller tiles lose more to per-FLOP
+// operand traffic than they gain in parallelism.  For F32 C with short K (one
+// K chunk per tile) the tile is C-traffic bound, and trading a ring stage for a
+// second epilogue staging slot per warp wins (+3-5 %).  Only a short M
+// (<= 128 rows) wastes enough of a 256-row tile to prefer a 1-CTA tile.
+int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
   if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
+  if (acc_type == GEMM_ACC_F32 && K <= 2048) return GEMM_CFG_PAIR_256x256_S5;
   return GEMM_CFG_PAIR_256x256;
 }
 
@@ -218,7 +224,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
 
   int cfg = opts ? opts->config : GEMM_CFG_AUTO;
   if (cfg < 0 || cfg >= GEMM_CFG_COUNT) return GEMM_ERR_INVALID_VALUE;
-  if (cfg == GEMM_CFG_AUTO) cfg = pick_config(M, N, di.sm_count);
+  if (cfg == GEMM_CFG_AUTO) cfg = pick_config(M, N, K, acc_type, di.sm_count);
   const ConfigDesc& cd = kConfigs[cfg];
   const int a = acc_type;
 
@@ -257,6 +263,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (hints < -1 || hints > 1) return GEMM_ERR_INVALID_VALUE;
   p.l2_hints = hints == 0 ? kDefaultL2Hints : (hints > 0 ? 1 : 0);
   p.debug_flags = opts ? opts->debug_flags : 0;
+  p.trace = opts ? static_cast<unsigned long long*>(opts->trace) : nullptr;
   const int pace = opts ? opts->epi_pace : 0;
   if (pace < -1 || pace > 1) return GEMM_ERR_INVALID_VALUE;
   p.epi_pace = pace == 0 ? kDefaultEpiPace : (pace > 0 ? 1 : 0);
@@ -339,11 +346,10 @@ gemm_status_t gemm_f16_host(int64_t M, int64_t N, int64_t K, const void* hA, int
 }
 
 int gemm_f16_pick_config(int64_t M, int64_t N, int64_t K, int acc_type) {
-  (void)K;
   if (acc_type != GEMM_ACC_F32 && acc_type != GEMM_ACC_F16) return -1;
   int dev = 0;
   if (device_ready(&dev) != GEMM_OK) return -1;
-  return pick_config(M, N, g_dev[dev].sm_count);
+  return pick_config(M, N, K, acc_type, g_dev[dev].sm_count);
 }
 
 gemm_status_t gemm_f16_config_info(int config, int acc_type, int* tile_m, int* tile_n, int* cta_group, int* stages,

@@ -57,6 +57,8 @@ struct GemmParams {
   int acc_bufs;                     // TMEM accumulator buffers in use (2 = epilogue overlaps MMA)
   int epi_pace;                     // 1: spread each tile's C_in/C_out traffic over half a K-chunk
                                     // interval instead of a burst synchronised across all SMs
+  unsigned long long* trace;        // DIAGNOSTIC ONLY (null normally): per-tile globaltimer stamps
+                                    // of CTA 0 (MMA start/end, epilogue drain/store), 8 per tile
   int l2_hints;                     // 1: TMA loads/stores carry L2 eviction-priority hints
                                     // (A evict_last: re-read by the next wave of tiles;
                                     //  C evict_first: streamed once)
@@ -88,6 +90,7 @@ struct KCfg {
   static_assert(RB == 128 || RB == 64, "staging rows are one 128B or 64B swizzle span");
   static constexpr int NOUT = CPW / CW;               // output chunks per warp per tile
   static constexpr int EPI_SLOTS = EPI_SLOTS_;
+  static constexpr int PRE = (EPI_SLOTS < NOUT) ? EPI_SLOTS : NOUT;   // C_in chunks loaded at tile start
   static constexpr int EPI_BUF = 32 * 128;            // 32 rows x up to 128 B
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = STAGES * A_BYTES;
@@ -242,10 +245,14 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
+      int it = 0;
+      for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
+        const bool tr = p.trace != nullptr && blockIdx.x == 0 && it < 64;
+        if (tr) p.trace[8 * it + 0] = globaltimer_ns();
         for (int ch = 0; ch < p.k_chunks; ++ch) {
           mbar_wait(acce_bar + 8 * acc, acc_phase ^ 1u);
           tc_fence_after();
+          if (tr && ch == 0) p.trace[8 * it + 1] = globaltimer_ns();
           const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
           const int kb0 = ch * p.kb_per_chunk;
           const int kb1 = min(kb0 + p.kb_per_chunk, p.k_blocks);
@@ -269,6 +276,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           }
           if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, 0x3);
           else umma_commit(accf_bar + 8 * acc);
+          if (tr && ch == p.k_chunks - 1) p.trace[8 * it + 2] = globaltimer_ns();
           if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1u; }
         }
       }
@@ -285,28 +293,47 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     const bool no_c = (p.debug_flags & 2) != 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint32_t out_ctr = 0;
     uint32_t slot_phase = 0;  // bit s = parity to wait for on slot s
     float racc[Cfg::CPW];
     uint64_t t_last = 0, chunk_ns = 0;   // arrival time of the last accumulator, interval
-    for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
+    int it = 0;
+    for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
+      const bool tr = p.trace != nullptr && blockIdx.x == 0 && ew == 0 && lane == 0 && it < 64;
       int tm, tn;
       tile_coords(tile, p, tm, tn);
       const int row0 = tm * BM * CG + static_cast<int>(rank) * BM + static_cast<int>(q) * 32;
       const int col0 = tn * BN + static_cast<int>(hcol);
+      if (tr) p.trace[8 * it + 3] = globaltimer_ns();
+      // C_in for the first PRE output chunks goes straight into the staging slots
+      // now, so its latency hides under this tile's MMAs (the slots were freed by
+      // the previous tile's stores).
+      if (lane == 0) {
+        bulk_wait_group_read<0>();
+#pragma unroll
+        for (int c = 0; c < Cfg::PRE; ++c) {
+          const uint32_t sbar = ebar0 + 8 * c;
+          if (!no_c) {
+            mbar_arrive_expect_tx(sbar, 32 * Cfg::RB);
+            tma_load_2d_hint(ebuf0 + c * Cfg::EPI_BUF, &tm_c, col0 + c * Cfg::CW, row0, sbar, pol_c);
+          } else {
+            mbar_arrive(sbar);
+          }
+        }
+      }
       // ---- promote each K chunk's TMEM partial sum into F32 registers (RN adds)
       const uint32_t t_lane = tmem_base + ((q * 32u) << 16) + hcol;
 #pragma unroll 1
       for (int ch = 0; ch < p.k_chunks; ++ch) {
-        if (ch == p.k_chunks - 1 && lane == 0 && !no_c) {
-          // C_in is needed right after this (last) chunk: pull it into L2 now, one
-          // chunk ahead, so it is neither evicted by a whole tile of operand traffic
-          // nor fetched from HBM in a burst synchronised across all SMs.
+        if (Cfg::PRE < Cfg::NOUT && ch == p.k_chunks - 1 && lane == 0 && !no_c) {
+          // the remaining C_in chunks are needed right after this (last) K chunk:
+          // pull them into L2 now, one chunk ahead, so they are neither evicted by
+          // a whole tile of operand traffic nor fetched from HBM in a burst.
 #pragma unroll 1
-          for (int c = 0; c < Cfg::NOUT; ++c) tma_prefetch_l2_2d(&tm_c, col0 + c * Cfg::CW, row0);
+          for (int c = Cfg::PRE; c < Cfg::NOUT; ++c) tma_prefetch_l2_2d(&tm_c, col0 + c * Cfg::CW, row0);
         }
         mbar_wait(accf_bar + 8 * acc, acc_phase);
         tc_fence_after();
+        if (tr && ch == p.k_chunks - 1) p.trace[8 * it + 4] = globaltimer_ns();
         if (p.epi_pace) {
           const uint64_t now = globaltimer_ns();
           if (t_last != 0) chunk_ns = now - t_last;
@@ -335,6 +362,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         }
         if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1u; }
       }
+      if (tr) p.trace[8 * it + 5] = globaltimer_ns();
       // ---- C_out = C_in + acc (F32 add, one rounding to the output type), TMA store.
       // Paced: output chunk c starts no earlier than c * chunk_ns / (2 * NOUT) after
       // the tile's last accumulator arrived, so the C traffic of all SMs (whose
@@ -347,22 +375,11 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           const uint64_t t_go = t_last + c * pace_ns;
           while (globaltimer_ns() < t_go) __nanosleep(256);
         }
-        const uint32_t slot = (Cfg::EPI_SLOTS == 1) ? 0u : (out_ctr & 1u);
+        const uint32_t slot = static_cast<uint32_t>(c % Cfg::EPI_SLOTS);
         const uint32_t sbuf = ebuf0 + slot * Cfg::EPI_BUF;
         const uint32_t sbar = ebar0 + 8 * slot;
         const int ccol = col0 + c * Cfg::CW;
         const bool manual = p.c_ragged && (ccol + Cfg::CW > p.N);
-        if (lane == 0) {
-          if constexpr (Cfg::EPI_SLOTS == 1) bulk_wait_group_read<0>();
-          else bulk_wait_group_read<1>();   // the store that last used this slot has read it
-          if (!no_c) {
-            mbar_arrive_expect_tx(sbar, 32 * Cfg::RB);
-            tma_load_2d_hint(sbuf, &tm_c, ccol, row0, sbar, pol_c);
-          } else {
-            mbar_arrive(sbar);
-          }
-        }
-        __syncwarp();
         mbar_wait(sbar, (slot_phase >> slot) & 1u);
         slot_phase ^= (1u << slot);
 #pragma unroll
@@ -412,8 +429,18 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         } else {
           __syncwarp();
         }
-        ++out_ctr;
+        if (c + Cfg::EPI_SLOTS < Cfg::NOUT && lane == 0) {
+          // refill this slot with chunk c + SLOTS once its store has read it
+          bulk_wait_group_read<0>();
+          if (!no_c) {
+            mbar_arrive_expect_tx(sbar, 32 * Cfg::RB);
+            tma_load_2d_hint(sbuf, &tm_c, ccol + Cfg::EPI_SLOTS * Cfg::CW, row0, sbar, pol_c);
+          } else {
+            mbar_arrive(sbar);
+          }
+        }
       }
+      if (tr) p.trace[8 * it + 6] = globaltimer_ns();
     }
     if (lane == 0) bulk_wait_group<0>();
   }
