@@ -328,11 +328,15 @@ def main():
         dA = torch.empty_like(A)
         dB = torch.empty_like(B)
 
+        e2e_launches = [0]
+
         def e2e_step():
             for m in modes:
                 g.gemm_f16_host(hA, hB, hC[m], dA, dB, dC[m], stream=stream)
+                e2e_launches[0] += g.last_launches()
         e2e_step()
         torch.cuda.synchronize()
+        e2e_launches[0] = 0
         if world > 1:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -352,7 +356,9 @@ def main():
         e2e = {"value": job_flops * len(modes) * args.e2e_steps / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "ms_per_step": e_ms / args.e2e_steps,
-               "path": "gemm_f16_host (C ABI): pinned host A,B,C -> H2D -> GEMM -> D2H, per mode"}
+               "path": "gemm_f16_host (C ABI): pinned host A,B,C -> row-block pipeline of H2D / GEMM / D2H "
+                       "on three streams, per mode",
+               "gpu_launches": e2e_launches[0]}
 
     # --------------------------------------------------------- optional NCCL all-gather of C (nshard)
     gather = None

@@ -112,11 +112,15 @@ gemm_status_t gemm_f16_ex(int64_t M, int64_t N, int64_t K,
 
 /*
  * gemm_f16_host: the same operation on HOST buffers (end-to-end path).
- * Enqueues on `stream`: host->device copies of A, B and C_in into the caller's
- * device scratch (dA/ldda, dB/lddb, dC/lddc, same element types and alignment
- * rules as gemm_f16), the GEMM, and the device->host copy of C_out back into
- * hC.  Host buffers should be page-locked for the copies to be asynchronous.
- * The caller synchronises `stream` before reading hC.
+ * Copies A, B and C_in into the caller's device scratch (dA/ldda, dB/lddb,
+ * dC/lddc: same element types and alignment rules as gemm_f16), runs the GEMM
+ * and copies C_out back into hC.  The work is pipelined over row blocks of
+ * >= 1024 rows (at most 8): copies in run on a library-owned H2D stream, the
+ * GEMMs on `stream`, copies out on a library-owned D2H stream, joined to
+ * `stream` by events -- the call is ordered after earlier work on `stream` and
+ * later work on `stream` is ordered after it.  Host buffers should be
+ * page-locked for the copies to be asynchronous.  The caller synchronises
+ * `stream` before reading hC.
  */
 gemm_status_t gemm_f16_host(int64_t M, int64_t N, int64_t K,
                             const void* hA, int64_t lda,
@@ -138,7 +142,7 @@ gemm_status_t gemm_f16_config_info(int config, int acc_type, int* tile_m, int* t
                                    int* cta_group, int* stages, int* smem_bytes);
 
 /* Number of kernel launches the last successful gemm_f16* call on this host
- * thread enqueued (0 or 1). */
+ * thread enqueued (gemm_f16: 0 or 1; gemm_f16_host: one per row block). */
 int gemm_f16_last_launches(void);
 
 const char* gemm_status_string(gemm_status_t s);

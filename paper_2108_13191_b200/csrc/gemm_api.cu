@@ -127,6 +127,23 @@ void init_device(int dev) {
   }
 }
 
+// Copy streams of the host-buffer path (created once per device, never destroyed).
+struct HostStreams {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaError_t err = cudaSuccess;
+};
+std::once_flag g_hs_once[kMaxDevices];
+HostStreams g_hs[kMaxDevices];
+
+HostStreams& host_streams(int dev) {
+  std::call_once(g_hs_once[dev], [dev]() {
+    HostStreams& h = g_hs[dev];
+    h.err = cudaStreamCreateWithFlags(&h.h2d, cudaStreamNonBlocking);
+    if (h.err == cudaSuccess) h.err = cudaStreamCreateWithFlags(&h.d2h, cudaStreamNonBlocking);
+  });
+  return g_hs[dev];
+}
+
 // ---------------------------------------------------------------- tensor maps
 using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -332,16 +349,61 @@ gemm_status_t gemm_f16_host(int64_t M, int64_t N, int64_t K, const void* hA, int
   int dev = 0;
   st = device_ready(&dev);
   if (st != GEMM_OK) return st;
+  HostStreams& hs = host_streams(dev);
+  if (hs.err != cudaSuccess) return cuda_fail(hs.err);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t csz = acc_type == GEMM_ACC_F32 ? 4 : 2;
-  cudaError_t e = cudaMemcpy2DAsync(dA, ldda * 2, hA, lda * 2, K * 2, M, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpy2DAsync(dB, lddb * 2, hB, ldb * 2, N * 2, K, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpy2DAsync(dC, lddc * csz, hC, ldc * csz, N * csz, M, cudaMemcpyHostToDevice, s);
+
+  // Row-block pipeline: B goes first (every block needs it); then block j's A
+  // and C_in rows are copied in on the H2D stream, its GEMM runs on the
+  // caller's stream, and its C_out rows go back on the D2H stream -- so the
+  // two copy directions and the tensor cores overlap.
+  const int64_t kMinRows = 1024;
+  int64_t nblk = std::min<int64_t>(8, std::max<int64_t>(1, M / kMinRows));
+  const int64_t rb = ((cdiv(M, nblk) + 255) / 256) * 256;
+  nblk = cdiv(M, rb);
+  cudaEvent_t ev_start, ev_done, ev_in[8], ev_gemm[8];
+  cudaError_t e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
+  for (int j = 0; j < nblk && e == cudaSuccess; ++j) {
+    e = cudaEventCreateWithFlags(&ev_in[j], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_gemm[j], cudaEventDisableTiming);
+  }
   if (e != cudaSuccess) return cuda_fail(e);
-  st = launch(M, N, K, dA, ldda, dB, lddb, dC, lddc, acc_type, s, nullptr);
+  e = cudaEventRecord(ev_start, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(hs.h2d, ev_start, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(hs.d2h, ev_start, 0);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(dB, lddb * 2, hB, ldb * 2, N * 2, K, cudaMemcpyHostToDevice, hs.h2d);
+  int launches = 0;
+  for (int64_t j = 0; j < nblk && e == cudaSuccess; ++j) {
+    const int64_t r0 = j * rb, mj = std::min(rb, M - r0);
+    const char* hAj = static_cast<const char*>(hA) + r0 * lda * 2;
+    char* dAj = static_cast<char*>(dA) + r0 * ldda * 2;
+    char* hCj = static_cast<char*>(hC) + r0 * ldc * csz;
+    char* dCj = static_cast<char*>(dC) + r0 * lddc * csz;
+    e = cudaMemcpy2DAsync(dAj, ldda * 2, hAj, lda * 2, K * 2, mj, cudaMemcpyHostToDevice, hs.h2d);
+    if (e == cudaSuccess) e = cudaMemcpy2DAsync(dCj, lddc * csz, hCj, ldc * csz, N * csz, mj, cudaMemcpyHostToDevice, hs.h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_in[j], hs.h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_in[j], 0);
+    if (e != cudaSuccess) break;
+    st = launch(mj, N, K, dAj, ldda, dB, lddb, dCj, lddc, acc_type, s, nullptr);
+    if (st != GEMM_OK) break;
+    ++launches;
+    e = cudaEventRecord(ev_gemm[j], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hs.d2h, ev_gemm[j], 0);
+    if (e == cudaSuccess) e = cudaMemcpy2DAsync(hCj, ldc * csz, dCj, lddc * csz, N * csz, mj, cudaMemcpyDeviceToHost, hs.d2h);
+  }
+  if (e == cudaSuccess && st == GEMM_OK) e = cudaEventRecord(ev_done, hs.d2h);
+  if (e == cudaSuccess && st == GEMM_OK) e = cudaStreamWaitEvent(s, ev_done, 0);
+  cudaEventDestroy(ev_start);
+  cudaEventDestroy(ev_done);
+  for (int j = 0; j < nblk; ++j) {
+    cudaEventDestroy(ev_in[j]);
+    cudaEventDestroy(ev_gemm[j]);
+  }
   if (st != GEMM_OK) return st;
-  e = cudaMemcpy2DAsync(hC, ldc * csz, dC, lddc * csz, N * csz, M, cudaMemcpyDeviceToHost, s);
   if (e != cudaSuccess) return cuda_fail(e);
+  t_last_launches = launches;
   return GEMM_OK;
 }
 
