@@ -80,6 +80,8 @@ typedef struct {
                     /* interval; -1: off                                                  */
   int ring_stages;  /* 0: all stages of the config; 1..stages: use a shallower smem ring   */
   int acc_bufs;     /* 0 or 2: double-buffered TMEM accumulator; 1: single (no overlap)   */
+  int k_serpentine; /* 0: default; 1: odd persistent iterations walk K backwards (L2      */
+                    /* reuse across waves; the K order then depends on the schedule); -1 off */
   void* trace;      /* DIAGNOSTIC ONLY, normally NULL: device buffer of 512 uint64 that   */
                     /* receives per-tile globaltimer stamps of CTA 0                      */
 } gemm_options_t;

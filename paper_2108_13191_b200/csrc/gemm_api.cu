@@ -23,6 +23,7 @@ using namespace g16;
 
 constexpr int kDefaultL2Hints = 1;
 constexpr int kDefaultEpiPace = 0;
+constexpr int kDefaultKSerpentine = 0;
 
 thread_local int t_last_cuda_error = 0;
 thread_local int t_last_launches = 0;
@@ -290,6 +291,9 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const int ab = opts ? opts->acc_bufs : 0;
   if (ab < 0 || ab > 2) return GEMM_ERR_INVALID_VALUE;
   p.acc_bufs = ab == 0 ? 2 : ab;
+  const int ks = opts ? opts->k_serpentine : 0;
+  if (ks < -1 || ks > 1) return GEMM_ERR_INVALID_VALUE;
+  p.k_serpentine = ks == 0 ? kDefaultKSerpentine : (ks > 0 ? 1 : 0);
 
   // persistent grid: one cluster per resident slot; an explicit max_clusters may
   // also exceed the resident slots (a non-persistent launch, for ablation)

@@ -53,6 +53,8 @@ struct GemmParams {
   long long ldc;                    // C leading dimension in elements
   int debug_flags;                  // DIAGNOSTIC ONLY (wrong results): 1 = no operand TMA after
                                     // the ring is filled once per tile, 2 = no C_in/C_out traffic
+  int k_serpentine;                 // 1: odd persistent iterations walk K backwards, so the next
+                                    // wave starts on the k-blocks the last one left hot in L2
   int ring_stages;                  // smem ring depth in use (1..STAGES; ablation of Sec 3.5)
   int acc_bufs;                     // TMEM accumulator buffers in use (2 = epilogue overlaps MMA)
   int epi_pace;                     // 1: spread each tile's C_in/C_out traffic over half a K-chunk
@@ -206,14 +208,17 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       const uint64_t pol_b = policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
+      int it = 0;
+      for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
         int tm, tn;
         tile_coords(tile, p, tm, tn);
         const int a_row = tm * BM * CG + static_cast<int>(rank) * BM;
         const int b_col = tn * BN + static_cast<int>(rank) * Cfg::BN_CTA;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        const bool backwards = p.k_serpentine && (it & 1);
+        for (int kbi = 0; kbi < p.k_blocks; ++kbi) {
+          const int kb = backwards ? p.k_blocks - 1 - kbi : kbi;
           mbar_wait(empty_bar + 8 * stage, phase ^ 1u);
-          if ((p.debug_flags & 1) && kb >= p.ring_stages) {
+          if ((p.debug_flags & 1) && kbi >= p.ring_stages) {
             if (rank == 0) mbar_arrive(full_bar + 8 * stage);
             if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
             continue;
