@@ -82,6 +82,8 @@ typedef struct {
   int acc_bufs;     /* 0 or 2: double-buffered TMEM accumulator; 1: single (no overlap)   */
   int k_serpentine; /* 0: default; 1: odd persistent iterations walk K backwards (L2      */
                     /* reuse across waves; the K order then depends on the schedule); -1 off */
+  int wait_hint_ns; /* 0: default; >0: suspend-time hint (ns) for the epilogue warps      */
+                    /* waiting for an accumulator; -1: plain polling                     */
   void* trace;      /* DIAGNOSTIC ONLY, normally NULL: device buffer of 512 uint64 that   */
                     /* receives per-tile globaltimer stamps of CTA 0                      */
 } gemm_options_t;

@@ -54,7 +54,8 @@ class _Options(ctypes.Structure):
     _fields_ = [("config", ctypes.c_int), ("max_clusters", ctypes.c_int), ("group_m", ctypes.c_int),
                 ("l2_hints", ctypes.c_int), ("debug_flags", ctypes.c_int), ("promote_k", ctypes.c_int),
                 ("epi_pace", ctypes.c_int), ("ring_stages", ctypes.c_int), ("acc_bufs", ctypes.c_int),
-                ("k_serpentine", ctypes.c_int), ("trace", ctypes.c_void_p)]
+                ("k_serpentine", ctypes.c_int), ("wait_hint_ns", ctypes.c_int),
+                ("trace", ctypes.c_void_p)]
 
 
 _lib = None
@@ -136,7 +137,7 @@ def _acc_of(C):
 
 def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int = 0, l2_hints: int = 0,
              debug_flags: int = 0, promote_k: int = 0, epi_pace: int = 0, ring_stages: int = 0,
-             acc_bufs: int = 0, k_serpentine: int = 0, trace=None):
+             acc_bufs: int = 0, k_serpentine: int = 0, wait_hint_ns: int = 0, trace=None):
     """In place: C += A @ B on the GPU (enqueued on `stream`, default: torch's current).
 
     A: (M, K) torch.float16 CUDA, B: (K, N) torch.float16 CUDA, C: (M, N) float32 or
@@ -158,7 +159,7 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
     cfg = CONFIGS[config] if isinstance(config, str) else int(config)
     opts = _Options(cfg, int(max_clusters), int(group_m), int(l2_hints), int(debug_flags), int(promote_k),
                     int(epi_pace), int(ring_stages), int(acc_bufs), int(k_serpentine),
-                    None if trace is None else ctypes.c_void_p(trace.data_ptr()))
+                    int(wait_hint_ns), None if trace is None else ctypes.c_void_p(trace.data_ptr()))
     with torch.cuda.device(C.device):
         st = lib.gemm_f16_ex(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
                              C.data_ptr(), _ld(C, "C"), acc, _stream_handle(stream, C.device),

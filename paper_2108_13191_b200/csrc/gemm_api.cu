@@ -24,6 +24,7 @@ using namespace g16;
 constexpr int kDefaultL2Hints = 1;
 constexpr int kDefaultEpiPace = 0;
 constexpr int kDefaultKSerpentine = 0;
+constexpr unsigned kDefaultWaitHintNs = 0;
 
 thread_local int t_last_cuda_error = 0;
 thread_local int t_last_launches = 0;
@@ -294,6 +295,9 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const int ks = opts ? opts->k_serpentine : 0;
   if (ks < -1 || ks > 1) return GEMM_ERR_INVALID_VALUE;
   p.k_serpentine = ks == 0 ? kDefaultKSerpentine : (ks > 0 ? 1 : 0);
+  const int wh = opts ? opts->wait_hint_ns : 0;
+  if (wh < -1) return GEMM_ERR_INVALID_VALUE;
+  p.wait_hint_ns = wh == 0 ? kDefaultWaitHintNs : (wh < 0 ? 0u : static_cast<unsigned>(wh));
 
   // persistent grid: one cluster per resident slot; an explicit max_clusters may
   // also exceed the resident slots (a non-persistent launch, for ablation)

@@ -53,6 +53,8 @@ struct GemmParams {
   long long ldc;                    // C leading dimension in elements
   int debug_flags;                  // DIAGNOSTIC ONLY (wrong results): 1 = no operand TMA after
                                     // the ring is filled once per tile, 2 = no C_in/C_out traffic
+  unsigned wait_hint_ns;            // suspend-time hint for the epilogue's accumulator waits
+                                    // (0 = plain polling); the producer/MMA always poll
   int k_serpentine;                 // 1: odd persistent iterations walk K backwards, so the next
                                     // wave starts on the k-blocks the last one left hot in L2
   int ring_stages;                  // smem ring depth in use (1..STAGES; ablation of Sec 3.5)
@@ -336,7 +338,8 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
 #pragma unroll 1
           for (int c = Cfg::PRE; c < Cfg::NOUT; ++c) tma_prefetch_l2_2d(&tm_c, col0 + c * Cfg::CW, row0);
         }
-        mbar_wait(accf_bar + 8 * acc, acc_phase);
+        if (p.wait_hint_ns) mbar_wait_sleep(accf_bar + 8 * acc, acc_phase, p.wait_hint_ns);
+        else mbar_wait(accf_bar + 8 * acc, acc_phase);
         tc_fence_after();
         if (tr && ch == p.k_chunks - 1) p.trace[8 * it + 4] = globaltimer_ns();
         if (p.epi_pace) {
