@@ -119,11 +119,11 @@ def _ld(t, name):
     return -(-max(t.size(1), 1) // per16) * per16
 
 
-def _stream_handle(stream, device):
+def _stream_handle(stream, device_index):
     import torch
     if stream is None:
-        stream = torch.cuda.current_stream(device)
-    return ctypes.c_void_p(stream.cuda_stream)
+        return torch._C._cuda_getCurrentRawStream(device_index)
+    return stream.cuda_stream
 
 
 def _acc_of(C):
@@ -151,19 +151,35 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
             raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
     if A.dtype != torch.float16 or B.dtype != torch.float16:
         raise TypeError("A and B must be torch.float16")
+    if A.device != C.device or B.device != C.device:
+        raise ValueError("A, B and C must be on the same CUDA device")
     acc = _acc_of(C)
     M, K = A.shape
     K2, N = B.shape
     if K2 != K or tuple(C.shape) != (M, N):
         raise ValueError(f"shape mismatch: A{tuple(A.shape)} B{tuple(B.shape)} C{tuple(C.shape)}")
     cfg = CONFIGS[config] if isinstance(config, str) else int(config)
-    opts = _Options(cfg, int(max_clusters), int(group_m), int(l2_hints), int(debug_flags), int(promote_k),
-                    int(epi_pace), int(ring_stages), int(acc_bufs), int(k_serpentine),
-                    int(wait_hint_ns), None if trace is None else ctypes.c_void_p(trace.data_ptr()))
-    with torch.cuda.device(C.device):
-        st = lib.gemm_f16_ex(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
-                             C.data_ptr(), _ld(C, "C"), acc, _stream_handle(stream, C.device),
-                             ctypes.byref(opts))
+    dev = C.device.index
+    cur = torch._C._cuda_getDevice()
+    ctx = torch.cuda.device(dev) if dev != cur else None
+    if ctx is not None:
+        ctx.__enter__()
+    try:
+        sh = _stream_handle(stream, dev)
+        if (cfg == 0 and not max_clusters and not group_m and not l2_hints and not debug_flags and not promote_k
+                and not epi_pace and not ring_stages and not acc_bufs and not k_serpentine and not wait_hint_ns
+                and trace is None):
+            st = lib.gemm_f16(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
+                              C.data_ptr(), _ld(C, "C"), acc, sh)
+        else:
+            opts = _Options(cfg, int(max_clusters), int(group_m), int(l2_hints), int(debug_flags), int(promote_k),
+                            int(epi_pace), int(ring_stages), int(acc_bufs), int(k_serpentine),
+                            int(wait_hint_ns), None if trace is None else ctypes.c_void_p(trace.data_ptr()))
+            st = lib.gemm_f16_ex(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
+                                 C.data_ptr(), _ld(C, "C"), acc, sh, ctypes.byref(opts))
+    finally:
+        if ctx is not None:
+            ctx.__exit__(None, None, None)
     _check(st)
     return C
 
@@ -184,7 +200,7 @@ def gemm_f16_host(hA, hB, hC, dA, dB, dC, stream=None):
         st = lib.gemm_f16_host(M, N, K, hA.data_ptr(), _ld(hA, "hA"), hB.data_ptr(), _ld(hB, "hB"),
                                hC.data_ptr(), _ld(hC, "hC"), acc,
                                dA.data_ptr(), _ld(dA, "dA"), dB.data_ptr(), _ld(dB, "dB"),
-                               dC.data_ptr(), _ld(dC, "dC"), _stream_handle(stream, dC.device))
+                               dC.data_ptr(), _ld(dC, "dC"), _stream_handle(stream, dC.device.index))
     _check(st)
     return hC
 

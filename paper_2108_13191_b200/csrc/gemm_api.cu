@@ -163,8 +163,31 @@ PFN_encodeTiled get_encode_fn() {
   return fn;
 }
 
+// Per-thread cache of encoded tensor maps: repeated calls on the same buffers
+// (training loops, benchmarks) skip cuTensorMapEncodeTiled.  The key is every
+// input of the encoding, so a hit returns exactly what encoding would.
+struct TmapKey {
+  const void* ptr;
+  int64_t rows, cols, ld;
+  int dt;
+  uint32_t box_cols, box_rows;
+  int l2, swz;
+  bool operator==(const TmapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && dt == o.dt &&
+           box_cols == o.box_cols && box_rows == o.box_rows && l2 == o.l2 && swz == o.swz;
+  }
+};
+constexpr int kTmapCache = 16;
+struct TmapCache {
+  TmapKey key[kTmapCache];
+  CUtensorMap map[kTmapCache];
+  bool valid[kTmapCache] = {};
+  int next = 0;
+};
+thread_local TmapCache t_tmap_cache;
+
 // 2-D row-major tensor (rows x cols, ld elements), box = box_cols x box_rows, 128B swizzle.
-bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* ptr, int64_t rows,
+bool encode_2d_uncached(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* ptr, int64_t rows,
                int64_t cols, int64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapL2promotion l2,
                CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   PFN_encodeTiled enc = get_encode_fn();
@@ -178,20 +201,47 @@ bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void*
   return r == CUDA_SUCCESS;
 }
 
+bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* ptr, int64_t rows,
+               int64_t cols, int64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapL2promotion l2,
+               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  TmapCache& c = t_tmap_cache;
+  const TmapKey k{ptr, rows, cols, ld, static_cast<int>(dt), box_cols, box_rows, static_cast<int>(l2),
+                  static_cast<int>(swz)};
+  for (int i = 0; i < kTmapCache; ++i) {
+    if (c.valid[i] && c.key[i] == k) {
+      *m = c.map[i];
+      return true;
+    }
+  }
+  if (!encode_2d_uncached(m, dt, esize, ptr, rows, cols, ld, box_cols, box_rows, l2, swz)) return false;
+  const int slot = c.next;
+  c.next = (c.next + 1) % kTmapCache;
+  c.key[slot] = k;
+  c.map[slot] = *m;
+  c.valid[slot] = true;
+  return true;
+}
+
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Shape -> configuration (the paper's per-size "best performing version",
 // P:903-905, as a fixed table so results stay deterministic).  Measured on B200
-// (profiles/r01/cfgsweep.md, profiles/r01/epilogue_slots.md): the 2-CTA 256x256
-// pair tile wins at every BASELINE shape from 2048^3 up, including the BERT
-// shapes and tails, even below one wave -- smaller tiles lose more to per-FLOP
-// operand traffic than they gain in parallelism.  For F32 C with short K (one
-// K chunk per tile) the tile is C-traffic bound, and trading a ring stage for a
-// second epilogue staging slot per warp wins (+3-5 %).  Only a short M
-// (<= 128 rows) wastes enough of a 256-row tile to prefer a 1-CTA tile.
+// (profiles/r01/cfgsweep.md, epilogue_slots.md, graph_small.md):
+//  * the 2-CTA 256x256 pair tile wins at every BASELINE shape from 2048^3 up,
+//    including the BERT shapes and tails, even below one wave -- smaller tiles
+//    lose more to per-FLOP operand traffic than they gain in parallelism;
+//  * with one K chunk per tile (K <= 2048) the tile is bound by its C traffic,
+//    and trading a ring stage for a second epilogue staging slot wins;
+//  * when the whole problem is under a third of a wave of pair tiles
+//    (e.g. 1024^3), fixed per-tile latency dominates and the 1-CTA 128x64 tile
+//    (more, shorter tiles) wins (GPU time from CUDA-graph replay);
+//  * a short M (<= 128 rows) wastes too much of a 256-row tile.
 int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
+  (void)acc_type;
   if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
-  if (acc_type == GEMM_ACC_F32 && K <= 2048) return GEMM_CFG_PAIR_256x256_S5;
+  const int64_t pair_tiles = cdiv(M, 256) * cdiv(N, 256);
+  if (3 * pair_tiles <= sm_count / 2) return GEMM_CFG_SOLO_128x64;
+  if (K <= 2048) return GEMM_CFG_PAIR_256x256_S5;
   return GEMM_CFG_PAIR_256x256;
 }
 

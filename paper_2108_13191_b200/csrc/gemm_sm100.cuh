@@ -173,6 +173,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
 
   const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const uint32_t lane = threadIdx.x & 31;
+  if (p.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) p.trace[8 * 62 + 0] = globaltimer_ns();
   const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
 
   if (warp == Cfg::W_PRODUCER && lane == 0) {
@@ -198,6 +199,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   tc_fence_after();
   uint32_t tmem_base;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot) : "memory");
+  if (p.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) p.trace[8 * 62 + 1] = globaltimer_ns();
 
   const int cluster = static_cast<int>(blockIdx.x) / CG;
   const int nclusters = static_cast<int>(gridDim.x) / CG;
@@ -451,6 +453,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       if (tr) p.trace[8 * it + 6] = globaltimer_ns();
     }
     if (lane == 0) bulk_wait_group<0>();
+    if (p.trace != nullptr && blockIdx.x == 0 && warp == 0 && lane == 0) p.trace[8 * 62 + 3] = globaltimer_ns();
   }
 
   // ===================== teardown =====================
@@ -461,6 +464,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, Cfg::TMEM_COLS);
   }
+  if (p.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) p.trace[8 * 62 + 2] = globaltimer_ns();
 }
 
 }  // namespace g16

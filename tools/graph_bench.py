@@ -1,0 +1,32 @@
+"""GPU-side time per GEMM for small shapes: R launches captured in one CUDA graph
+and replayed (removes host enqueue cost), per config."""
+import os, sys, json, statistics
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import torch, synth
+import paper_2108_13191_b200 as g
+shapes = [(256, 256, 256), (512, 512, 512), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 1024, 1024), (2048, 2048, 512)]
+R = 20
+for (M, N, K) in shapes:
+    for mode in ("f32", "f16"):
+        A = torch.from_numpy(synth.uniform_f16(0, 0, M, K)).cuda()
+        B = torch.from_numpy(synth.uniform_f16(0, 1, K, N)).cuda()
+        C = torch.from_numpy((synth.uniform_f32 if mode == "f32" else synth.uniform_f16)(0, 2, M, N)).cuda()
+        row = {"shape": [M, N, K], "mode": mode, "auto": g.pick_config(M, N, K, 0 if mode == "f32" else 1)}
+        for cfg in (1, 2, 4, 5, 6):
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(3): g.gemm_f16(A, B, C, config=cfg)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s):
+                for _ in range(R): g.gemm_f16(A, B, C, config=cfg)
+            graph.replay(); torch.cuda.synchronize()
+            ts = []
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+                e0.record(); graph.replay(); e1.record(); torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) / R * 1000)
+            us = statistics.median(ts)
+            row[f"cfg{cfg}_us"] = round(us, 2)
+            row[f"cfg{cfg}_tflops"] = round(2 * M * N * K / us / 1e6, 1)
+        print(json.dumps(row), flush=True)

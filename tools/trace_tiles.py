@@ -15,8 +15,17 @@ g.gemm_f16(A, B, C, trace=tr, **kw)
 torch.cuda.synchronize()
 t = tr.cpu().numpy().reshape(64, 8)
 t0 = t[0, 0]
+e = t[62]
+print(f"CTA0: entry {(e[0]-t0)/1000:.2f} us, setup done {(e[1]-t0)/1000:.2f}, epilogue stores drained {(e[3]-t0)/1000:.2f}, exit {(e[2]-t0)/1000:.2f}")
+import time
+torch.cuda.synchronize()
+t_h = time.perf_counter()
+for _ in range(200): g.gemm_f16(A, B, C, **kw)
+t_h = (time.perf_counter() - t_h) / 200
+torch.cuda.synchronize()
+print(f"host enqueue time per gemm_f16 call (python + C ABI + launch): {t_h*1e6:.1f} us")
 print(f"{M}x{N}x{K} {mode} {kw}: columns (us from MMA start of tile 0): mma_begin acce_ok mma_end | epi_begin accfull_last drained stored")
-for i in range(64):
+for i in range(62):
     if t[i, 0] == 0: break
     r = [(x - t0) / 1000 if x else float('nan') for x in t[i, :7]]
     print(f"tile {i:2d}: " + " ".join(f"{x:8.2f}" for x in r[:3]) + " | " + " ".join(f"{x:8.2f}" for x in r[3:7]))
