@@ -256,8 +256,12 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       uint32_t acc_phase = 0;
       int it = 0;
       for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
-        const bool tr = p.trace != nullptr && blockIdx.x == 0 && it < 64;
-        if (tr) p.trace[8 * it + 0] = globaltimer_ns();
+        const bool tr = p.trace != nullptr && blockIdx.x == 0 && it < 60;
+        uint64_t clk0 = 0;
+        if (tr) {
+          p.trace[8 * it + 0] = globaltimer_ns();
+          clk0 = clock64();
+        }
         for (int ch = 0; ch < p.k_chunks; ++ch) {
           mbar_wait(acce_bar + 8 * acc, acc_phase ^ 1u);
           tc_fence_after();
@@ -285,7 +289,10 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           }
           if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, 0x3);
           else umma_commit(accf_bar + 8 * acc);
-          if (tr && ch == p.k_chunks - 1) p.trace[8 * it + 2] = globaltimer_ns();
+          if (tr && ch == p.k_chunks - 1) {
+            p.trace[8 * it + 2] = globaltimer_ns();
+            p.trace[8 * it + 7] = clock64() - clk0;   // SM cycles of this tile (MMA warp)
+          }
           if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1u; }
         }
       }
@@ -307,7 +314,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     uint64_t t_last = 0, chunk_ns = 0;   // arrival time of the last accumulator, interval
     int it = 0;
     for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
-      const bool tr = p.trace != nullptr && blockIdx.x == 0 && ew == 0 && lane == 0 && it < 64;
+      const bool tr = p.trace != nullptr && blockIdx.x == 0 && ew == 0 && lane == 0 && it < 60;
       int tm, tn;
       tile_coords(tile, p, tm, tn);
       const int row0 = tm * BM * CG + static_cast<int>(rank) * BM + static_cast<int>(q) * 32;

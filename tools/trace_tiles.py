@@ -28,4 +28,7 @@ print(f"{M}x{N}x{K} {mode} {kw}: columns (us from MMA start of tile 0): mma_begi
 for i in range(62):
     if t[i, 0] == 0: break
     r = [(x - t0) / 1000 if x else float('nan') for x in t[i, :7]]
-    print(f"tile {i:2d}: " + " ".join(f"{x:8.2f}" for x in r[:3]) + " | " + " ".join(f"{x:8.2f}" for x in r[3:7]))
+    cyc = int(t[i, 7]); ns = t[i, 2] - t[i, 0]
+    kb = -(-K // 64)
+    print(f"tile {i:2d}: " + " ".join(f"{x:8.2f}" for x in r[:3]) + " | " + " ".join(f"{x:8.2f}" for x in r[3:7])
+          + f" | {cyc} cyc, SM clock {cyc/max(ns,1):.3f} GHz, {cyc/kb:.0f} cyc per k-block")
