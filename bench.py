@@ -318,6 +318,26 @@ def main():
         except (OSError, ValueError):
             traffic = None
 
+    # --------------------------------------------------------- SM clock seen by the kernel itself
+    # NVML's clock reading lags over a ~50 ms window; one extra traced launch (after the
+    # timed region, not timed) reports clock64 / globaltimer of CTA 0's MMA warp per tile.
+    kernel_clock = None
+    try:
+        tr = torch.zeros(512, dtype=torch.int64, device=dev)
+        with torch.cuda.stream(stream):
+            step()
+            g.gemm_f16(A, B, C[modes[0]], stream=stream, config=args.config, trace=tr)
+        torch.cuda.synchronize()
+        t = tr.cpu().numpy().reshape(64, 8)
+        ghz = [t[i, 7] / (t[i, 2] - t[i, 0]) for i in range(60) if t[i, 0] and t[i, 2] > t[i, 0] and t[i, 7]]
+        if ghz:
+            kernel_clock = {"sm_mhz_median": round(1000 * float(statistics.median(ghz)), 1),
+                            "sm_mhz_min": round(1000 * float(min(ghz)), 1), "sm_mhz_max": round(1000 * float(max(ghz)), 1),
+                            "tiles": len(ghz), "how": "clock64/globaltimer of CTA 0's MMA warp per tile, one traced "
+                                                      "launch right after the timed region"}
+    except Exception as ex:  # tracing is diagnostic only
+        kernel_clock = {"error": str(ex)[:120]}
+
     # --------------------------------------------------------- e2e through the host-buffer C ABI
     e2e = None
     if not args.no_e2e:
@@ -433,7 +453,9 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": dict(clk.summary(), kernel_measured=kernel_clock,
+                           note="NVML sm_mhz is sampled every 2 ms but lags; kernel_measured is the SM "
+                                "clock the GEMM actually ran at (power-capped)"),
             "parity": parity,
             "allgather": gather,
         }

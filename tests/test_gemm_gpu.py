@@ -233,7 +233,8 @@ def test_promotion_bounds_long_k_error(g):
 @pytest.mark.parametrize("kw", [
     {"ring_stages": 1}, {"ring_stages": 2}, {"acc_bufs": 1}, {"acc_bufs": 1, "ring_stages": 1},
     {"group_m": 1}, {"group_m": 3}, {"l2_hints": -1}, {"epi_pace": -1}, {"max_clusters": 1000},
-    {"config": "pair_256x256_s5"}, {"config": "solo_128x256", "ring_stages": 1, "acc_bufs": 1},
+    {"config": "pair_256x256_s5"}, {"config": "pair_256x256_s4"}, {"config": "solo_128x256", "ring_stages": 1, "acc_bufs": 1},
+    {"k_serpentine": 1, "max_clusters": 2}, {"wait_hint_ns": 20000}, {"epi_pace": 1},
 ])
 def test_ablation_knobs_keep_parity(g, kw):
     """Every ablation switch (used by tools/ablation.py) is a scheduling choice only:
@@ -290,3 +291,17 @@ def test_cuda_graph_capture_replay(g):
         graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(cap.view(torch.int32), eager.view(torch.int32))
+
+
+def test_trace_option_records_tiles(g):
+    """The diagnostic trace hook fills per-tile stamps without changing results."""
+    import torch
+    M, N, K = 1024, 1024, 4096
+    A, B, C, gA, gB, gC = device_problem(M, N, K, "f32", seed=14)
+    tr = torch.zeros(512, dtype=torch.int64, device="cuda")
+    _run(g, gA, gB, gC, config="pair_256x256", trace=tr)
+    ex, _ = oracle_full(A, B, C)
+    check(gC.result(), ex, A, B, "f32", K, "traced")
+    t = tr.cpu().numpy().reshape(64, 8)
+    assert t[0, 0] > 0 and t[0, 2] > t[0, 0] and t[0, 7] > 0   # MMA begin/end stamps, cycles
+    assert t[62, 0] > 0 and t[62, 2] >= t[62, 0]               # kernel entry/exit of CTA 0
