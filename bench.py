@@ -149,16 +149,14 @@ def oracle_sample_rate(n: int, modes, budget_s: float, seed: int = 0):
     A = synth.uniform_f16(seed, synth.MATRIX_A, n, n)
     B = synth.uniform_f16(seed, synth.MATRIX_B, n, n)
     Cs = {m: (synth.uniform_f32 if m == "f32" else synth.uniform_f16)(seed, synth.MATRIX_C, n, n) for m in modes}
-    # t(rows) ~ a + b*rows (a: decoding B once per call); fit from two probes
-    ts = []
-    for probe_rows in (2, 8):
-        t0 = time.perf_counter()
-        for m in modes:
-            oracle.gemm(A, B, Cs[m], rows=np.arange(probe_rows))
-        ts.append(time.perf_counter() - t0)
-    b = max((ts[1] - ts[0]) / 6.0, 1e-6)
-    a = max(ts[0] - 2 * b, 0.0)
-    rows = int(max(2, min(n, (budget_s - a) / b)))
+    # OpenMP runs one row per thread, so the cost grows in rounds of `threads`
+    # rows: time one full round, then take as many rounds as fit the budget.
+    threads = max(1, oracle.num_threads())
+    t0 = time.perf_counter()
+    for m in modes:
+        oracle.gemm(A, B, Cs[m], rows=np.arange(min(n, threads)))
+    t_round = max(time.perf_counter() - t0, 1e-6)
+    rows = int(min(n, max(1, int(budget_s / t_round)) * threads))
     sel = np.linspace(0, n - 1, rows).astype(np.int64)
     t0 = time.perf_counter()
     for m in modes:
@@ -183,14 +181,16 @@ def run_reference(args):
     A = synth.uniform_f16(0, synth.MATRIX_A, n, n)
     B = synth.uniform_f16(0, synth.MATRIX_B, n, n)
     Cs = {m: (synth.uniform_f32 if m == "f32" else synth.uniform_f16)(0, synth.MATRIX_C, n, n) for m in modes}
-    # size each step so warmup + steps fit in a few minutes
+    # size each step so warmup + steps fit in a few minutes (rows run one per
+    # OpenMP thread, so a step is a whole number of thread rounds)
     total_budget = 150.0
     per_step = total_budget / max(1, args.steps + args.warmup)
+    threads = max(1, oracle.num_threads())
     t0 = time.perf_counter()
     for m in modes:
-        oracle.gemm(A, B, Cs[m], rows=np.arange(2))
-    t2 = (time.perf_counter() - t0) / 2.0
-    rows = int(max(1, min(n, per_step / max(t2, 1e-6))))
+        oracle.gemm(A, B, Cs[m], rows=np.arange(min(n, threads)))
+    t_round = max(time.perf_counter() - t0, 1e-6)
+    rows = int(min(n, max(1, int(per_step / t_round)) * threads))
     sel = np.linspace(0, n - 1, rows).astype(np.int64)
     for _ in range(args.warmup):
         for m in modes:

@@ -61,7 +61,8 @@ typedef enum {
   GEMM_CFG_SOLO_128x64 = 5,  /* cta_group::1, UMMA 128x64x16                */
   GEMM_CFG_PAIR_256x256_S5 = 6, /* as PAIR_256x256, 5 stages, 2 epilogue staging slots per warp */
   GEMM_CFG_PAIR_256x256_S4 = 7, /* as PAIR_256x256, 4 stages, 3 epilogue staging slots per warp */
-  GEMM_CFG_COUNT = 8
+  GEMM_CFG_PAIR_256x256_K128 = 8, /* as PAIR_256x256 with 128-deep K stages (3 stages)        */
+  GEMM_CFG_COUNT = 9
 } gemm_config_t;
 
 typedef struct {
@@ -75,7 +76,8 @@ typedef struct {
                     /* operand loads after the ring fills, 2 = skip C_in/C_out traffic   */
   int promote_k;    /* K elements per TMEM accumulation chunk before the partial sum is  */
                     /* added into F32 registers (RN): 0 = default 2048, -1 = never       */
-                    /* (one TMEM chain per tile), else a positive multiple of 64         */
+                    /* (one TMEM chain per tile), else a positive multiple of the        */
+                    /* config's K stage depth (64, or 128 for PAIR_256x256_K128)          */
   int epi_pace;     /* 0: default (off); 1: pace each tile's C traffic over half a K-chunk */
                     /* interval; -1: off                                                  */
   int ring_stages;  /* 0: all stages of the config; 1..stages: use a shallower smem ring   */

@@ -31,6 +31,7 @@ CONFIGS = {
     "solo_128x64": 5,
     "pair_256x256_s5": 6,
     "pair_256x256_s4": 7,
+    "pair_256x256_k128": 8,
 }
 _STATUS = {0: "GEMM_OK", 1: "GEMM_ERR_INVALID_VALUE", 2: "GEMM_ERR_MISALIGNED",
            3: "GEMM_ERR_UNSUPPORTED_DEVICE", 4: "GEMM_ERR_CUDA"}

@@ -43,11 +43,13 @@ using Cfg6F32 = KCfg<2, 256, 5, false, 2>;
 using Cfg6F16 = KCfg<2, 256, 5, true, 2>;
 using Cfg7F32 = KCfg<2, 256, 4, false, 3>;
 using Cfg7F16 = KCfg<2, 256, 4, true, 3>;
+using Cfg8F32 = KCfg<2, 256, 3, false, 1, 128>;
+using Cfg8F16 = KCfg<2, 256, 3, true, 1, 128>;
 
 using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const GemmParams);
 
 struct ConfigDesc {
-  int cta_group, tile_n, stages, threads;
+  int cta_group, tile_n, stages, threads, bk;
   int smem[2];      // [acc_type]
   int c_box_cols[2];  // epilogue staging box width (elements)
   int c_row_bytes[2]; // 128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B
@@ -56,13 +58,13 @@ struct ConfigDesc {
 
 template <class C32, class C16>
 constexpr ConfigDesc make_desc() {
-  return ConfigDesc{C32::CG, C32::BN, C32::STAGES, C32::THREADS,
+  return ConfigDesc{C32::CG, C32::BN, C32::STAGES, C32::THREADS, C32::BK,
                     {C32::SMEM_BYTES, C16::SMEM_BYTES}, {C32::CW, C16::CW}, {C32::RB, C16::RB},
                     {&gemm_f16_sm100_kernel<C32>, &gemm_f16_sm100_kernel<C16>}};
 }
 
 const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
-    ConfigDesc{0, 0, 0, 0, {0, 0}, {0, 0}, {0, 0}, {nullptr, nullptr}},
+    ConfigDesc{0, 0, 0, 0, 0, {0, 0}, {0, 0}, {0, 0}, {nullptr, nullptr}},
     make_desc<Cfg1F32, Cfg1F16>(),
     make_desc<Cfg2F32, Cfg2F16>(),
     make_desc<Cfg3F32, Cfg3F16>(),
@@ -70,6 +72,7 @@ const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
     make_desc<Cfg5F32, Cfg5F16>(),
     make_desc<Cfg6F32, Cfg6F16>(),
     make_desc<Cfg7F32, Cfg7F16>(),
+    make_desc<Cfg8F32, Cfg8F16>(),
 };
 
 // K elements accumulated in TMEM before the partial sum is promoted to F32
@@ -226,23 +229,24 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Shape -> configuration (the paper's per-size "best performing version",
 // P:903-905, as a fixed table so results stay deterministic).  Measured on B200
-// (profiles/r01/cfgsweep.md, epilogue_slots.md, graph_small.md):
+// (profiles/r01/cfgsweep.md, epilogue_slots.md, graph_small.md, stage_depth.md):
 //  * the 2-CTA 256x256 pair tile wins at every BASELINE shape from 2048^3 up,
 //    including the BERT shapes and tails, even below one wave -- smaller tiles
 //    lose more to per-FLOP operand traffic than they gain in parallelism;
-//  * with one K chunk per tile (K <= 2048) the tile is bound by its C traffic,
-//    and trading a ring stage for a second epilogue staging slot wins;
+//  * 128-deep K stages (3 x 64 KB) beat 64-deep ones (6 x 32 KB) by 2-4 %:
+//    half the barrier/commit round trips per FLOP and fewer DRAM re-reads;
+//  * for F32 C with one K chunk per tile (K <= 2048) the tile is bound by its C
+//    traffic, and a second epilogue staging slot per warp (5 x 32 KB ring) wins;
 //  * when the whole problem is under a third of a wave of pair tiles
 //    (e.g. 1024^3), fixed per-tile latency dominates and the 1-CTA 128x64 tile
 //    (more, shorter tiles) wins (GPU time from CUDA-graph replay);
 //  * a short M (<= 128 rows) wastes too much of a 256-row tile.
 int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
-  (void)acc_type;
   if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
   const int64_t pair_tiles = cdiv(M, 256) * cdiv(N, 256);
   if (3 * pair_tiles <= sm_count / 2) return GEMM_CFG_SOLO_128x64;
-  if (K <= 2048) return GEMM_CFG_PAIR_256x256_S5;
-  return GEMM_CFG_PAIR_256x256;
+  if (acc_type == GEMM_ACC_F32 && K <= 2048) return GEMM_CFG_PAIR_256x256_S5;
+  return GEMM_CFG_PAIR_256x256_K128;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -317,10 +321,10 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n;
   if (tiles > 0x7fffffffLL) return GEMM_ERR_INVALID_VALUE;
   p.num_tiles = static_cast<int>(tiles);
-  p.k_blocks = static_cast<int>(cdiv(K, 64));
+  p.k_blocks = static_cast<int>(cdiv(K, cd.bk));
   const int promote = opts ? opts->promote_k : 0;
-  if (promote < -1 || (promote > 0 && promote % 64 != 0)) return GEMM_ERR_INVALID_VALUE;
-  p.kb_per_chunk = promote == -1 ? p.k_blocks : (promote == 0 ? kDefaultPromoteK : promote) / 64;
+  if (promote < -1 || (promote > 0 && promote % cd.bk != 0)) return GEMM_ERR_INVALID_VALUE;
+  p.kb_per_chunk = promote == -1 ? p.k_blocks : (promote == 0 ? kDefaultPromoteK : promote) / cd.bk;
   p.k_chunks = static_cast<int>(cdiv(p.k_blocks, p.kb_per_chunk));
   p.group_m = (opts && opts->group_m > 0) ? opts->group_m : 8;
   if (opts && opts->group_m < 0) return GEMM_ERR_INVALID_VALUE;

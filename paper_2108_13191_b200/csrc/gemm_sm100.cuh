@@ -68,21 +68,25 @@ struct GemmParams {
                                     //  C evict_first: streamed once)
 };
 
-template <int CG_, int BN_, int STAGES_, bool OUT_F16_, int EPI_SLOTS_ = 1>
+template <int CG_, int BN_, int STAGES_, bool OUT_F16_, int EPI_SLOTS_ = 1, int BK_ = 64>
 struct KCfg {
   static constexpr int CG = CG_;            // CTAs per MMA (cta_group)
   static constexpr int BN = BN_;            // UMMA N (tile columns)
   static constexpr int STAGES = STAGES_;
   static constexpr bool OUT_F16 = OUT_F16_;
   static constexpr int BM = 128;            // rows per CTA (TMEM lanes)
-  static constexpr int BK = 64;             // K per stage = one 128B swizzle span of F16
+  static constexpr int BK = BK_;            // K per stage: KH 64-deep (128 B) swizzle spans of F16
+  static constexpr int KH = BK / 64;
+  static_assert(BK == 64 || BK == 128, "K per stage");
   static constexpr int UMMA_K = 16;
   static constexpr int BN_CTA = BN / CG;    // B columns staged per CTA
   static_assert(BN_CTA % 64 == 0, "B is staged in 64-column (128 B) swizzle atoms");
   static_assert(BN % 64 == 0 && BN <= 256, "UMMA N");
-  static constexpr int A_BYTES = BM * BK * 2;         // 16 KB
-  static constexpr int B_ATOM_BYTES = 64 * BK * 2;    // 64 cols x 64 k = 8 KB
-  static constexpr int B_BYTES = BN_CTA * BK * 2;
+  static constexpr int A_HALF_BYTES = BM * 64 * 2;   // 16 KB: 128 rows x one 64-deep K span
+  static constexpr int A_BYTES = KH * A_HALF_BYTES;
+  static constexpr int B_ATOM_BYTES = 64 * 64 * 2;    // 64 cols x 64 k = 8 KB
+  static constexpr int B_HALF_BYTES = BN_CTA * 64 * 2;
+  static constexpr int B_BYTES = KH * B_HALF_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int ACC_COLS = BN;                 // one accumulator buffer
   static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
@@ -231,16 +235,22 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           const uint32_t fb = full_leader + 8 * stage;
           const uint32_t a_dst = sA + stage * Cfg::A_BYTES;
           const uint32_t b_dst = sB + stage * Cfg::B_BYTES;
-          if constexpr (CG == 2) {
-            tma_load_2d_pair_hint(a_dst, &tm_a, kb * BK, a_row, fb, pol_a);
 #pragma unroll
-            for (int h = 0; h < Cfg::BN_CTA / 64; ++h)
-              tma_load_2d_pair_hint(b_dst + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h, kb * BK, fb, pol_b);
-          } else {
-            tma_load_2d_hint(a_dst, &tm_a, kb * BK, a_row, fb, pol_a);
+          for (int kh = 0; kh < Cfg::KH; ++kh) {
+            const int kc = kb * BK + 64 * kh;
+            if constexpr (CG == 2) {
+              tma_load_2d_pair_hint(a_dst + kh * Cfg::A_HALF_BYTES, &tm_a, kc, a_row, fb, pol_a);
 #pragma unroll
-            for (int h = 0; h < Cfg::BN_CTA / 64; ++h)
-              tma_load_2d_hint(b_dst + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h, kb * BK, fb, pol_b);
+              for (int h = 0; h < Cfg::BN_CTA / 64; ++h)
+                tma_load_2d_pair_hint(b_dst + kh * Cfg::B_HALF_BYTES + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h,
+                                      kc, fb, pol_b);
+            } else {
+              tma_load_2d_hint(a_dst + kh * Cfg::A_HALF_BYTES, &tm_a, kc, a_row, fb, pol_a);
+#pragma unroll
+              for (int h = 0; h < Cfg::BN_CTA / 64; ++h)
+                tma_load_2d_hint(b_dst + kh * Cfg::B_HALF_BYTES + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h, kc,
+                                 fb, pol_b);
+            }
           }
           if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
         }
@@ -277,10 +287,11 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
 #pragma unroll
             for (int k = 0; k < BK / Cfg::UMMA_K; ++k) {
               // A (K-major): advance 16 elements = 32 B inside the 128B swizzle row.
-              const uint64_t adesc = desc_sw128(a_s + 32 * k, 16, 1024);
+              const uint64_t adesc = desc_sw128(a_s + (k >> 2) * Cfg::A_HALF_BYTES + 32 * (k & 3), 16, 1024);
               // B (MN-major): advance 16 k-rows = 2 swizzle atoms of 8 rows x 128 B;
               // 64-column groups are B_ATOM_BYTES apart (LBO), 8-row groups 1 KB (SBO).
-              const uint64_t bdesc = desc_sw128(b_s + 2048 * k, Cfg::B_ATOM_BYTES, 1024);
+              const uint64_t bdesc = desc_sw128(b_s + (k >> 2) * Cfg::B_HALF_BYTES + 2048 * (k & 3),
+                                                Cfg::B_ATOM_BYTES, 1024);
               umma_f16<CG>(d_tmem, adesc, bdesc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             }
             if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, 0x3);
