@@ -117,6 +117,34 @@ gemm_status_t gemm_f16_ex(int64_t M, int64_t N, int64_t K,
                           const gemm_options_t* opts);
 
 /*
+ * gemm_f16_gather: one rank's share of an N-sharded C += A.B, fused with the
+ * all-gather of C.  Every rank holds a full M x N
+ * buffer C; this rank owns the column slab [n0, n0 + nr):
+ *     C[:, n0:n0+nr] <- C[:, n0:n0+nr] + A . B_r
+ * with C_in read from its own C, and each finished C tile is stored by the
+ * epilogue (TMA) into C AND into every peers[d][:, n0:n0+nr], d < n_peers --
+ * so the gather overlaps the math tile by tile instead of following it.
+ *   A, lda       binary16 M x K (replicated on every rank)
+ *   B_r, ldb     binary16 K x nr, this rank's column slab of B, ldb >= nr
+ *   C, ldc       this rank's full M x N buffer (float or binary16), read+written
+ *   peers        n_peers (<= 7) device addresses of the other ranks' full C
+ *                buffers with the same shape, ld and type, mapped into this
+ *                process (NVLink peer / symmetric-memory pointers) or plain
+ *                buffers on this device; written only in columns [n0, n0+nr)
+ * Alignment as gemm_f16, plus n0*sizeof(C elem) a multiple of 16 bytes (slab
+ * boundaries at multiples of 8 columns).  Writes to peers are complete when the
+ * kernel completes; the caller orders readers after it (e.g. a cross-rank
+ * barrier after synchronising `stream`).
+ */
+gemm_status_t gemm_f16_gather(int64_t M, int64_t N, int64_t K,
+                              const void* A, int64_t lda,
+                              const void* B_r, int64_t ldb,
+                              int64_t n0, int64_t nr,
+                              void* C, int64_t ldc,
+                              void* const* peers, int n_peers,
+                              int acc_type, void* stream);
+
+/*
  * gemm_f16_host: the same operation on HOST buffers (end-to-end path).
  * Copies A, B and C_in into the caller's device scratch (dA/ldda, dB/lddb,
  * dC/lddc: same element types and alignment rules as gemm_f16), runs the GEMM

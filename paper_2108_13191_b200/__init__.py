@@ -17,7 +17,7 @@ import os
 
 from . import _build
 
-__all__ = ["gemm_f16", "gemm_f16_host", "GemmError", "ACC_F32", "ACC_F16", "CONFIGS",
+__all__ = ["gemm_f16", "gemm_f16_gather", "gemm_f16_host", "GemmError", "ACC_F32", "ACC_F16", "CONFIGS",
            "config_info", "pick_config", "library_path", "load_library", "last_launches"]
 
 ACC_F32 = 0
@@ -36,7 +36,7 @@ CONFIGS = {
 _STATUS = {0: "GEMM_OK", 1: "GEMM_ERR_INVALID_VALUE", 2: "GEMM_ERR_MISALIGNED",
            3: "GEMM_ERR_UNSUPPORTED_DEVICE", 4: "GEMM_ERR_CUDA"}
 
-EXPORTED_SYMBOLS = ("gemm_f16", "gemm_f16_ex", "gemm_f16_host", "gemm_f16_pick_config",
+EXPORTED_SYMBOLS = ("gemm_f16", "gemm_f16_ex", "gemm_f16_gather", "gemm_f16_host", "gemm_f16_pick_config",
                     "gemm_f16_config_info", "gemm_f16_last_launches", "gemm_status_string",
                     "gemm_last_cuda_error")
 
@@ -85,6 +85,8 @@ def load_library(build_if_missing: bool = True):
     lib.gemm_f16.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, ci, vp]
     lib.gemm_f16_ex.restype = ci
     lib.gemm_f16_ex.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, ci, vp, ctypes.POINTER(_Options)]
+    lib.gemm_f16_gather.restype = ci
+    lib.gemm_f16_gather.argtypes = [i64, i64, i64, vp, i64, vp, i64, i64, i64, vp, i64, ctypes.POINTER(vp), ci, ci, vp]
     lib.gemm_f16_host.restype = ci
     lib.gemm_f16_host.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, ci, vp, i64, vp, i64, vp, i64, vp]
     lib.gemm_f16_pick_config.restype = ci
@@ -178,6 +180,41 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
                             int(wait_hint_ns), None if trace is None else ctypes.c_void_p(trace.data_ptr()))
             st = lib.gemm_f16_ex(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
                                  C.data_ptr(), _ld(C, "C"), acc, sh, ctypes.byref(opts))
+    finally:
+        if ctx is not None:
+            ctx.__exit__(None, None, None)
+    _check(st)
+    return C
+
+
+def gemm_f16_gather(A, B_r, C, n0: int, peers=(), stream=None):
+    """This rank's share of an N-sharded C += A.B fused with the all-gather of C.
+
+    C: this rank's full (M, N) buffer (float32 or float16, CUDA); the rank owns
+    columns [n0, n0 + B_r.shape[1]).  C[:, n0:n0+nr] += A @ B_r, and each finished
+    tile is also stored into every peer buffer at the same columns.  `peers`:
+    device addresses (ints) or tensors of the other ranks' full C buffers, same
+    shape / dtype / row stride, mapped into this process (e.g. torch symmetric
+    memory `buffer_ptrs`) or other buffers on this device.  At most 7.
+    """
+    import torch
+    lib = load_library()
+    acc = _acc_of(C)
+    M, K = A.shape
+    K2, nr = B_r.shape
+    if K2 != K or C.shape[0] != M or n0 < 0 or n0 + nr > C.shape[1]:
+        raise ValueError("shape mismatch")
+    ptrs = [int(x.data_ptr()) if hasattr(x, "data_ptr") else int(x) for x in peers]
+    arr = (ctypes.c_void_p * max(1, len(ptrs)))(*ptrs)
+    dev = C.device.index
+    ctx = torch.cuda.device(dev) if dev != torch._C._cuda_getDevice() else None
+    if ctx is not None:
+        ctx.__enter__()
+    try:
+        st = lib.gemm_f16_gather(M, C.shape[1], K, A.data_ptr(), _ld(A, "A"), B_r.data_ptr(), _ld(B_r, "B_r"),
+                                 int(n0), int(nr), C.data_ptr(), _ld(C, "C"),
+                                 ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)), len(ptrs), acc,
+                                 _stream_handle(stream, dev))
     finally:
         if ctx is not None:
             ctx.__exit__(None, None, None)

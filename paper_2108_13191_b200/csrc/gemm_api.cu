@@ -45,8 +45,11 @@ using Cfg7F32 = KCfg<2, 256, 4, false, 3>;
 using Cfg7F16 = KCfg<2, 256, 4, true, 3>;
 using Cfg8F32 = KCfg<2, 256, 3, false, 1, 128>;
 using Cfg8F16 = KCfg<2, 256, 3, true, 1, 128>;
+// gemm_f16_gather: the 128-deep pair tile with peer stores compiled in
+using CfgGF32 = KCfg<2, 256, 3, false, 1, 128, true>;
+using CfgGF16 = KCfg<2, 256, 3, true, 1, 128, true>;
 
-using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const GemmParams);
+using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const GemmParams, const PeerMaps);
 
 struct ConfigDesc {
   int cta_group, tile_n, stages, threads, bk;
@@ -74,6 +77,7 @@ const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
     make_desc<Cfg7F32, Cfg7F16>(),
     make_desc<Cfg8F32, Cfg8F16>(),
 };
+const ConfigDesc kGatherConfig = make_desc<CfgGF32, CfgGF16>();
 
 // K elements accumulated in TMEM before the partial sum is promoted to F32
 // registers (R4): 2048 keeps the truncation error near 2.4e-6.
@@ -85,7 +89,7 @@ struct DeviceInfo {
   gemm_status_t status = GEMM_OK;
   int cuda_error = 0;
   int sm_count = 0;
-  int max_clusters[GEMM_CFG_COUNT][2] = {};
+  int max_clusters[GEMM_CFG_COUNT + 1][2] = {};   // [GEMM_CFG_COUNT] = the gather config
 };
 std::once_flag g_dev_once[kMaxDevices];
 DeviceInfo g_dev[kMaxDevices];
@@ -98,9 +102,9 @@ void init_device(int dev) {
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
   if (major != 10 || minor != 0) { d.status = GEMM_ERR_UNSUPPORTED_DEVICE; return; }
-  for (int c = 1; c < GEMM_CFG_COUNT; ++c) {
+  for (int c = 1; c <= GEMM_CFG_COUNT; ++c) {
     for (int a = 0; a < 2; ++a) {
-      const ConfigDesc& cd = kConfigs[c];
+      const ConfigDesc& cd = c == GEMM_CFG_COUNT ? kGatherConfig : kConfigs[c];
       e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.fn[a]),
                                cudaFuncAttributeMaxDynamicSharedMemorySize, cd.smem[a]);
       if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
@@ -289,7 +293,8 @@ gemm_status_t device_ready(int* dev_out) {
 }
 
 gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb,
-                     void* C, int64_t ldc, int acc_type, cudaStream_t stream, const gemm_options_t* opts) {
+                     void* C, int64_t ldc, int acc_type, cudaStream_t stream, const gemm_options_t* opts,
+                     void* const* peers = nullptr, int n_peers = 0) {
   int dev = 0;
   gemm_status_t st = device_ready(&dev);
   if (st != GEMM_OK) return st;
@@ -298,7 +303,8 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   int cfg = opts ? opts->config : GEMM_CFG_AUTO;
   if (cfg < 0 || cfg >= GEMM_CFG_COUNT) return GEMM_ERR_INVALID_VALUE;
   if (cfg == GEMM_CFG_AUTO) cfg = pick_config(M, N, K, acc_type, di.sm_count);
-  const ConfigDesc& cd = kConfigs[cfg];
+  if (n_peers > 0) cfg = GEMM_CFG_COUNT;   // fused gather: the peer-store build of PAIR_256x256_K128
+  const ConfigDesc& cd = cfg == GEMM_CFG_COUNT ? kGatherConfig : kConfigs[cfg];
   const int a = acc_type;
 
   CUtensorMap tm_a, tm_b, tm_c;
@@ -310,8 +316,20 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 cd.c_row_bytes[a] == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return cuda_fail(cudaErrorInvalidValue);
+  PeerMaps pm;
+  std::memset(&pm, 0, sizeof(pm));
+  for (int d = 0; d < n_peers; ++d) {
+    if (!encode_2d(&pm.m[d], acc_type == GEMM_ACC_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   acc_type == GEMM_ACC_F32 ? 4 : 2, peers[d], M, N, ldc, static_cast<uint32_t>(cd.c_box_cols[a]), 32,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   cd.c_row_bytes[a] == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
+      return cuda_fail(cudaErrorInvalidValue);
+  }
 
   GemmParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.n_peers = n_peers;
+  for (int d = 0; d < n_peers; ++d) p.peer_ptr[d] = peers[d];
   p.M = static_cast<int>(M);
   p.N = static_cast<int>(N);
   p.K = static_cast<int>(K);
@@ -374,7 +392,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
     lc.attrs = attr;
     lc.numAttrs = 1;
   }
-  cudaError_t e = cudaLaunchKernelEx(&lc, cd.fn[a], tm_a, tm_b, tm_c, p);
+  cudaError_t e = cudaLaunchKernelEx(&lc, cd.fn[a], tm_a, tm_b, tm_c, p, pm);
   if (e != cudaSuccess) return cuda_fail(e);
   t_last_launches = 1;
   return GEMM_OK;
@@ -396,6 +414,30 @@ gemm_status_t gemm_f16_ex(int64_t M, int64_t N, int64_t K, const void* A, int64_
 gemm_status_t gemm_f16(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb,
                        void* C, int64_t ldc, int acc_type, void* stream) {
   return gemm_f16_ex(M, N, K, A, lda, B, ldb, C, ldc, acc_type, stream, nullptr);
+}
+
+gemm_status_t gemm_f16_gather(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B_r,
+                              int64_t ldb, int64_t n0, int64_t nr, void* C, int64_t ldc, void* const* peers,
+                              int n_peers, int acc_type, void* stream) {
+  t_last_launches = 0;
+  if (n0 < 0 || nr < 0 || N < 0 || n0 + nr > N) return GEMM_ERR_INVALID_VALUE;
+  if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && !peers)) return GEMM_ERR_INVALID_VALUE;
+  const int64_t csz = acc_type == GEMM_ACC_F32 ? 4 : 2;
+  if (acc_type != GEMM_ACC_F32 && acc_type != GEMM_ACC_F16) return GEMM_ERR_INVALID_VALUE;
+  if (ldc < std::max<int64_t>(1, N)) return GEMM_ERR_INVALID_VALUE;
+  // this rank's slab [n0, n0 + nr) of C, and of every peer buffer (same shape and ld)
+  char* C_slab = C ? static_cast<char*>(C) + n0 * csz : nullptr;
+  bool no_work = false;
+  gemm_status_t st = validate(M, nr, K, A, lda, B_r, ldb, C_slab, ldc, acc_type, &no_work);
+  if (st != GEMM_OK || no_work) return st;
+  void* peer_slab[kMaxPeers];
+  for (int d = 0; d < n_peers; ++d) {
+    if (!peers[d]) return GEMM_ERR_INVALID_VALUE;
+    peer_slab[d] = static_cast<char*>(peers[d]) + n0 * csz;
+    if (!aligned16(peer_slab[d])) return GEMM_ERR_MISALIGNED;
+  }
+  return launch(M, nr, K, A, lda, B_r, ldb, C_slab, ldc, acc_type, static_cast<cudaStream_t>(stream), nullptr,
+                peer_slab, n_peers);
 }
 
 gemm_status_t gemm_f16_host(int64_t M, int64_t N, int64_t K, const void* hA, int64_t lda, const void* hB,

@@ -39,6 +39,13 @@
 
 namespace g16 {
 
+// Extra destinations of the C tile (fused N-shard all-gather, gemm_f16_gather):
+// every finished C chunk is TMA-stored to the local C and to each peer buffer.
+constexpr int kMaxPeers = 7;
+struct PeerMaps {
+  CUtensorMap m[kMaxPeers];
+};
+
 struct GemmParams {
   int M, N, K;
   int tiles_m, tiles_n, num_tiles;  // tiles of (128*CG) x BN
@@ -50,6 +57,8 @@ struct GemmParams {
                                     // whole 16-byte granule past column N-1, so the chunk
                                     // holding column N-1 is stored element-wise instead
   void* c_ptr;                      // C base (used only by that ragged-N store path)
+  int n_peers;                      // extra destinations of C_out (0 = plain GEMM)
+  void* peer_ptr[kMaxPeers];        // their bases, for the ragged-N store path
   long long ldc;                    // C leading dimension in elements
   int debug_flags;                  // DIAGNOSTIC ONLY (wrong results): 1 = no operand TMA after
                                     // the ring is filled once per tile, 2 = no C_in/C_out traffic
@@ -68,12 +77,13 @@ struct GemmParams {
                                     //  C evict_first: streamed once)
 };
 
-template <int CG_, int BN_, int STAGES_, bool OUT_F16_, int EPI_SLOTS_ = 1, int BK_ = 64>
+template <int CG_, int BN_, int STAGES_, bool OUT_F16_, int EPI_SLOTS_ = 1, int BK_ = 64, bool PEERS_ = false>
 struct KCfg {
   static constexpr int CG = CG_;            // CTAs per MMA (cta_group)
   static constexpr int BN = BN_;            // UMMA N (tile columns)
   static constexpr int STAGES = STAGES_;
   static constexpr bool OUT_F16 = OUT_F16_;
+  static constexpr bool PEERS = PEERS_;     // epilogue also stores C to p.n_peers peer buffers
   static constexpr int BM = 128;            // rows per CTA (TMEM lanes)
   static constexpr int BK = BK_;            // K per stage: KH 64-deep (128 B) swizzle spans of F16
   static constexpr int KH = BK / 64;
@@ -160,7 +170,8 @@ __global__ void __launch_bounds__(352, 1)
 gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                       const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_c,
-                      const GemmParams p) {
+                      const __grid_constant__ GemmParams p,
+                      const __grid_constant__ PeerMaps peers) {
   constexpr int CG = Cfg::CG, BN = Cfg::BN, STAGES = Cfg::STAGES, BM = Cfg::BM, BK = Cfg::BK;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -184,6 +195,8 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     prefetch_tmap(&tm_a);
     prefetch_tmap(&tm_b);
     prefetch_tmap(&tm_c);
+    if constexpr (Cfg::PEERS)
+      for (int d = 0; d < p.n_peers; ++d) prefetch_tmap(&peers.m[d]);
   }
   if (warp == Cfg::W_MMA && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -417,16 +430,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           if constexpr (!Cfg::OUT_F16) {
             const float4 ci = lds128(addr);
             const float o0 = ci.x + a[0], o1 = ci.y + a[1], o2 = ci.z + a[2], o3 = ci.w + a[3];
-            if (!manual) {
-              sts128(addr, o0, o1, o2, o3);
-            } else if (grow < p.M) {
-              float* dst = static_cast<float*>(p.c_ptr) + static_cast<long long>(grow) * p.ldc;
-              const int cb = ccol + 4 * j;
-              const float o[4] = {o0, o1, o2, o3};
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (cb + e < p.N) dst[cb + e] = o[e];
-            }
+            sts128(addr, o0, o1, o2, o3);
           } else {
             const uint4 ci = lds128u(addr);
             const float2 c0 = f16x2_to_f32(ci.x), c1 = f16x2_to_f32(ci.y);
@@ -435,16 +439,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
             const uint32_t o1 = cvt_f16x2_rn(c1.x + a[2], c1.y + a[3]);
             const uint32_t o2 = cvt_f16x2_rn(c2.x + a[4], c2.y + a[5]);
             const uint32_t o3 = cvt_f16x2_rn(c3.x + a[6], c3.y + a[7]);
-            if (!manual) {
-              sts128u(addr, o0, o1, o2, o3);
-            } else if (grow < p.M) {
-              uint16_t* dst = static_cast<uint16_t*>(p.c_ptr) + static_cast<long long>(grow) * p.ldc;
-              const int cb = ccol + 8 * j;
-              const uint32_t o[4] = {o0, o1, o2, o3};
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                if (cb + e < p.N) dst[cb + e] = static_cast<uint16_t>(o[e >> 1] >> (16 * (e & 1)));
-            }
+            sts128u(addr, o0, o1, o2, o3);
           }
         }
         if (!manual && !no_c) {
@@ -452,10 +447,36 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           __syncwarp();
           if (lane == 0) {
             tma_store_2d_hint(&tm_c, ccol, row0, sbuf, pol_c);
+            // fused all-gather: the same staged chunk goes to every peer's C
+            if constexpr (Cfg::PEERS)
+              for (int d = 0; d < p.n_peers; ++d) tma_store_2d_hint(&peers.m[d], ccol, row0, sbuf, pol_c);
             bulk_commit_group();
           }
         } else {
           __syncwarp();
+          if (manual && !no_c && grow < p.M) {
+            // ragged N edge: element-wise stores of this thread's row, read back
+            // from the staged chunk, clipped at column N, to C and every peer
+#pragma unroll 1
+            for (int j = 0; j < Cfg::RB / 16; ++j) {
+              const uint4 v = lds128u(sbuf + swz<Cfg::RB>(lane, static_cast<uint32_t>(j)));
+              const uint32_t o[4] = {v.x, v.y, v.z, v.w};
+              constexpr int EPU = 16 / Cfg::ESIZE;   // elements per 16-byte unit
+              const int cb = ccol + EPU * j;
+              const int nd = Cfg::PEERS ? p.n_peers : 0;
+#pragma unroll 1
+              for (int d = -1; d < nd; ++d) {
+                char* base = static_cast<char*>(d < 0 ? p.c_ptr : p.peer_ptr[d]) +
+                             (static_cast<long long>(grow) * p.ldc + cb) * Cfg::ESIZE;
+#pragma unroll
+                for (int e = 0; e < EPU; ++e) {
+                  if (cb + e >= p.N) break;
+                  if constexpr (Cfg::ESIZE == 4) reinterpret_cast<uint32_t*>(base)[e] = o[e];
+                  else reinterpret_cast<uint16_t*>(base)[e] = static_cast<uint16_t>(o[e >> 1] >> (16 * (e & 1)));
+                }
+              }
+            }
+          }
         }
         if (c + Cfg::EPI_SLOTS < Cfg::NOUT && lane == 0) {
           // refill this slot with chunk c + SLOTS once its store has read it

@@ -96,3 +96,34 @@ def gemm_batched_one_per_gpu(problems, rank: int, world: int, compute: Callable 
         compute(A, B, C, **kw)
         done.append(i)
     return done
+
+
+def gemm_nshard_gather(A, B_r, C_full, n_slabs, rank: int, peer_ptrs=(), **kw):
+    """Fused N-shard + all-gather (one kernel): this rank computes its column slab
+    of C_full (C_in read from its own C_full) and its epilogue stores each finished
+    tile into C_full and into every peer's C_full (`peer_ptrs`: device addresses
+    of the other ranks' full C buffers, e.g. from `symmetric_c_buffer`).  After
+    every rank's kernel has completed (synchronise, then a cross-rank barrier),
+    every C_full holds the whole result -- the gather overlapped the math instead
+    of following it (SURVEY.md 8(e) NEXT #3)."""
+    from . import gemm_f16_gather
+    n0, n1 = n_slabs[rank]
+    if n1 == n0:
+        return C_full
+    return gemm_f16_gather(A, B_r, C_full, n0, peers=peer_ptrs, **kw)
+
+
+def symmetric_c_buffer(M: int, N: int, dtype, group=None):
+    """Allocate this rank's full C in torch symmetric memory and return
+    (tensor, [peer device addresses of the other ranks' buffers], handle).
+    Needs NVLink-connected GPUs in one node (CUDA IPC); the handle's barrier()
+    orders readers after all ranks' writers."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+
+    t = symm_mem.empty((M, N), dtype=dtype, device=torch.device("cuda", torch.cuda.current_device()))
+    hdl = symm_mem.rendezvous(t, group=group if group is not None else dist.group.WORLD)
+    me = hdl.rank
+    peers = [int(p) for r, p in enumerate(hdl.buffer_ptrs) if r != me]
+    return t, peers, hdl

@@ -90,3 +90,59 @@ def test_fake_rank_nshard_bitwise(g):
             out[:, n0:n1] = C_r
         torch.cuda.synchronize()
         assert torch.equal(out.view(torch.int32), full.view(torch.int32)), P
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+def test_fused_gather_simulated_ranks(g, P, acc):
+    """gemm_f16_gather on one GPU with P full-size C buffers standing in for the
+    P ranks' memories: rank r computes its slab and stores it into all P buffers.
+    Afterwards every buffer equals the unsharded C += A.B (oracle parity), and
+    bitwise equals the plain GEMM in the same tile configuration."""
+    import torch
+    from paper_2108_13191_b200 import dist as gdist
+    M, N, K = 600, 1000, 2200    # ragged M; N slabs of 8-column multiples incl. a ragged last one
+    A, B, C = synth.problem(M, N, K, acc, seed=30 + P)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    bufs = [torch.from_numpy(C.copy()).cuda() for _ in range(P)]
+    slabs = gdist.column_slabs(N, P, align=8)
+    for r in range(P):
+        n0, n1 = slabs[r]
+        B_r = dB[:, n0:n1].contiguous()
+        peers = [bufs[j] for j in range(P) if j != r]
+        gdist.gemm_nshard_gather(dA, B_r, bufs[r], slabs, r, peer_ptrs=peers)
+    torch.cuda.synchronize()
+    ex, _ = oracle.gemm(A, B, C)
+    ref = torch.from_numpy(C.copy()).cuda()
+    g.gemm_f16(dA, dB, ref, config="pair_256x256_k128")
+    for r in range(P):
+        check(bufs[r].cpu().numpy(), ex, A, B, acc, K, f"gather P={P} buffer {r}")
+    ibits = torch.int32 if acc == "f32" else torch.int16
+    for r in range(P):   # per-element K order is independent of the N tiling
+        assert torch.equal(bufs[r].view(ibits), ref.view(ibits)), r
+
+
+def test_symmetric_buffer_rendezvous_single_rank(g):
+    """The symmetric-memory plumbing of the fused gather runs on a 1-rank NCCL
+    group (no peers): allocation, rendezvous, and the fused kernel on the buffer."""
+    import os, socket
+    import torch
+    import torch.distributed as dist
+    from paper_2108_13191_b200 import dist as gdist
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        M, N, K = 512, 768, 640
+        A, B, C = synth.problem(M, N, K, "f32", seed=44)
+        t, peers, hdl = gdist.symmetric_c_buffer(M, N, torch.float32)
+        assert peers == []
+        t.copy_(torch.from_numpy(C))
+        slabs = gdist.column_slabs(N, 1)
+        gdist.gemm_nshard_gather(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), t, slabs, 0, peers)
+        torch.cuda.synchronize()
+        hdl.barrier()
+        ex, _ = oracle.gemm(A, B, C)
+        check(t.cpu().numpy(), ex, A, B, "f32", K, "symmetric buffer")
+    finally:
+        dist.destroy_process_group()
