@@ -10,7 +10,9 @@ import paper_2108_13191_b200 as g
 
 n = int(os.environ.get("N", "8192"))
 mode = os.environ.get("MODE", "f32")
-rounds = int(os.environ.get("ROUNDS", "4")); reps = int(os.environ.get("REPS", "10"))
+rounds = int(os.environ.get("ROUNDS", "12")); reps = int(os.environ.get("REPS", "4"))
+import random
+rng = random.Random(0)
 naive = dict(config="solo_128x256", ring_stages=1, acc_bufs=1, group_m=1, l2_hints=-1, promote_k=-1, epi_pace=-1)
 cumulative = [
     ("naive: 1-CTA 128x256, 1-stage ring, single TMEM acc, row-major order", dict(naive)),
@@ -19,17 +21,17 @@ cumulative = [
     ("+ 2-CTA pair 256x256 (cta_group::2), 6 stages", dict(naive, config="pair_256x256", ring_stages=0, acc_bufs=0)),
     ("+ grouped raster (group_m=8)", dict(naive, config="pair_256x256", ring_stages=0, acc_bufs=0, group_m=0)),
     ("+ L2 eviction hints", dict(naive, config="pair_256x256", ring_stages=0, acc_bufs=0, group_m=0, l2_hints=0)),
-    ("+ K-chunk promotion to F32 registers (accuracy)", dict(config="pair_256x256", epi_pace=-1)),
-    ("+ paced epilogue (= shipped default)", dict()),
+    ("+ K-chunk promotion to F32 registers (accuracy)", dict(config="pair_256x256")),
+    ("+ 128-deep K stages (= shipped default)", dict()),
 ]
 removals = [
-    ("full - ring (1 stage)", dict(ring_stages=1)),
-    ("full - ring (2 stages)", dict(ring_stages=2)),
-    ("full - ring (3 stages)", dict(ring_stages=3)),
-    ("full - ring (4 stages)", dict(ring_stages=4)),
+    ("full (shipped default), again", dict()),
+    ("full - ring (1 x 128-deep stage)", dict(ring_stages=1)),
+    ("full - ring (2 x 128-deep stages)", dict(ring_stages=2)),
     ("full - TMEM double buffer", dict(acc_bufs=1)),
     ("full - persistence (one cluster per tile)", dict(max_clusters=100000)),
-    ("full - 2-CTA (1-CTA 128x256)", dict(config="solo_128x256")),
+    ("full - 2-CTA (1-CTA 128x256, 64-deep)", dict(config="solo_128x256")),
+    ("full - 128-deep stages (64-deep, 6 stages)", dict(config="pair_256x256")),
     ("full - raster (row-major tiles)", dict(group_m=1)),
     ("full - L2 hints", dict(l2_hints=-1)),
     ("full - promotion", dict(promote_k=-1)),
@@ -43,7 +45,10 @@ for name, kw in variants:
     g.gemm_f16(A, B, C, **kw)
 torch.cuda.synchronize()
 for r in range(rounds):
-    for i, (name, kw) in enumerate(variants):
+    order = list(range(len(variants)))
+    rng.shuffle(order)   # no variant always runs in the same (thermal) position of a round
+    for i in order:
+        name, kw = variants[i]
         s, e = torch.cuda.Event(True), torch.cuda.Event(True)
         s.record()
         for _ in range(reps): g.gemm_f16(A, B, C, **kw)
@@ -52,4 +57,5 @@ for r in range(rounds):
 for i, (name, kw) in enumerate(variants):
     ms = statistics.median(res[i])
     print(json.dumps({"variant": name, "kwargs": kw, "n": n, "mode": mode, "ms": round(ms, 4),
+                      "ms_p25": round(sorted(res[i])[len(res[i]) // 4], 4), "ms_p75": round(sorted(res[i])[3 * len(res[i]) // 4], 4),
                       "tflops": round(2 * n ** 3 / ms / 1e9, 1), "group": "cumulative" if i < len(cumulative) else "removal"}), flush=True)
