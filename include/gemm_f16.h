@@ -86,6 +86,8 @@ typedef struct {
                     /* reuse across waves; the K order then depends on the schedule); -1 off */
   int wait_hint_ns; /* 0: default; >0: suspend-time hint (ns) for the epilogue warps      */
                     /* waiting for an accumulator; -1: plain polling                     */
+  int c_row_prefetch; /* 0: default; 1: at tile start each epilogue warp L2-prefetches its */
+                    /* whole C_in region in full rows; -1: off                           */
   void* trace;      /* DIAGNOSTIC ONLY, normally NULL: device buffer of 512 uint64 that   */
                     /* receives per-tile globaltimer stamps of CTA 0                      */
 } gemm_options_t;

@@ -56,7 +56,7 @@ class _Options(ctypes.Structure):
                 ("l2_hints", ctypes.c_int), ("debug_flags", ctypes.c_int), ("promote_k", ctypes.c_int),
                 ("epi_pace", ctypes.c_int), ("ring_stages", ctypes.c_int), ("acc_bufs", ctypes.c_int),
                 ("k_serpentine", ctypes.c_int), ("wait_hint_ns", ctypes.c_int),
-                ("trace", ctypes.c_void_p)]
+                ("c_row_prefetch", ctypes.c_int), ("trace", ctypes.c_void_p)]
 
 
 _lib = None
@@ -140,7 +140,8 @@ def _acc_of(C):
 
 def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int = 0, l2_hints: int = 0,
              debug_flags: int = 0, promote_k: int = 0, epi_pace: int = 0, ring_stages: int = 0,
-             acc_bufs: int = 0, k_serpentine: int = 0, wait_hint_ns: int = 0, trace=None):
+             acc_bufs: int = 0, k_serpentine: int = 0, wait_hint_ns: int = 0, c_row_prefetch: int = 0,
+             trace=None):
     """In place: C += A @ B on the GPU (enqueued on `stream`, default: torch's current).
 
     A: (M, K) torch.float16 CUDA, B: (K, N) torch.float16 CUDA, C: (M, N) float32 or
@@ -171,13 +172,14 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
         sh = _stream_handle(stream, dev)
         if (cfg == 0 and not max_clusters and not group_m and not l2_hints and not debug_flags and not promote_k
                 and not epi_pace and not ring_stages and not acc_bufs and not k_serpentine and not wait_hint_ns
-                and trace is None):
+                and not c_row_prefetch and trace is None):
             st = lib.gemm_f16(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
                               C.data_ptr(), _ld(C, "C"), acc, sh)
         else:
             opts = _Options(cfg, int(max_clusters), int(group_m), int(l2_hints), int(debug_flags), int(promote_k),
                             int(epi_pace), int(ring_stages), int(acc_bufs), int(k_serpentine),
-                            int(wait_hint_ns), None if trace is None else ctypes.c_void_p(trace.data_ptr()))
+                            int(wait_hint_ns), int(c_row_prefetch),
+                            None if trace is None else ctypes.c_void_p(trace.data_ptr()))
             st = lib.gemm_f16_ex(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
                                  C.data_ptr(), _ld(C, "C"), acc, sh, ctypes.byref(opts))
     finally:

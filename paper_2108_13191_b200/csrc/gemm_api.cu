@@ -25,6 +25,7 @@ constexpr int kDefaultL2Hints = 1;
 constexpr int kDefaultEpiPace = 0;
 constexpr int kDefaultKSerpentine = 0;
 constexpr unsigned kDefaultWaitHintNs = 0;
+constexpr int kDefaultCRowPrefetch = 0;
 
 thread_local int t_last_cuda_error = 0;
 thread_local int t_last_launches = 0;
@@ -49,7 +50,8 @@ using Cfg8F16 = KCfg<2, 256, 3, true, 1, 128>;
 using CfgGF32 = KCfg<2, 256, 3, false, 1, 128, true>;
 using CfgGF16 = KCfg<2, 256, 3, true, 1, 128, true>;
 
-using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const GemmParams, const PeerMaps);
+using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const GemmParams, const PeerMaps,
+                          const CUtensorMap);
 
 struct ConfigDesc {
   int cta_group, tile_n, stages, threads, bk;
@@ -316,6 +318,13 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 cd.c_row_bytes[a] == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return cuda_fail(cudaErrorInvalidValue);
+  // C_in L2-prefetch map: one box = an epilogue warp's whole region (32 rows x tile_n/2
+  // columns), unswizzled -- it only drives cp.async.bulk.prefetch, never smem
+  CUtensorMap tm_cpf;
+  if (!encode_2d(&tm_cpf, acc_type == GEMM_ACC_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                 acc_type == GEMM_ACC_F32 ? 4 : 2, C, M, N, ldc, static_cast<uint32_t>(cd.tile_n / 2), 32,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cuda_fail(cudaErrorInvalidValue);
   PeerMaps pm;
   std::memset(&pm, 0, sizeof(pm));
   for (int d = 0; d < n_peers; ++d) {
@@ -370,6 +379,9 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const int wh = opts ? opts->wait_hint_ns : 0;
   if (wh < -1) return GEMM_ERR_INVALID_VALUE;
   p.wait_hint_ns = wh == 0 ? kDefaultWaitHintNs : (wh < 0 ? 0u : static_cast<unsigned>(wh));
+  const int crp = opts ? opts->c_row_prefetch : 0;
+  if (crp < -1 || crp > 1) return GEMM_ERR_INVALID_VALUE;
+  p.c_row_prefetch = crp == 0 ? kDefaultCRowPrefetch : (crp > 0 ? 1 : 0);
 
   // persistent grid: one cluster per resident slot; an explicit max_clusters may
   // also exceed the resident slots (a non-persistent launch, for ablation)
@@ -392,7 +404,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
     lc.attrs = attr;
     lc.numAttrs = 1;
   }
-  cudaError_t e = cudaLaunchKernelEx(&lc, cd.fn[a], tm_a, tm_b, tm_c, p, pm);
+  cudaError_t e = cudaLaunchKernelEx(&lc, cd.fn[a], tm_a, tm_b, tm_c, p, pm, tm_cpf);
   if (e != cudaSuccess) return cuda_fail(e);
   t_last_launches = 1;
   return GEMM_OK;

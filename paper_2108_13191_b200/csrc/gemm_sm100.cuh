@@ -62,6 +62,8 @@ struct GemmParams {
   long long ldc;                    // C leading dimension in elements
   int debug_flags;                  // DIAGNOSTIC ONLY (wrong results): 1 = no operand TMA after
                                     // the ring is filled once per tile, 2 = no C_in/C_out traffic
+  int c_row_prefetch;               // 1: at tile start, one L2 prefetch per epilogue warp of its
+                                    // whole C_in region (full 32 x CPW rows: long DRAM bursts)
   unsigned wait_hint_ns;            // suspend-time hint for the epilogue's accumulator waits
                                     // (0 = plain polling); the producer/MMA always poll
   int k_serpentine;                 // 1: odd persistent iterations walk K backwards, so the next
@@ -171,7 +173,8 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                       const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_c,
                       const __grid_constant__ GemmParams p,
-                      const __grid_constant__ PeerMaps peers) {
+                      const __grid_constant__ PeerMaps peers,
+                      const __grid_constant__ CUtensorMap tm_cpf) {
   constexpr int CG = Cfg::CG, BN = Cfg::BN, STAGES = Cfg::STAGES, BM = Cfg::BM, BK = Cfg::BK;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -348,6 +351,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       // now, so its latency hides under this tile's MMAs (the slots were freed by
       // the previous tile's stores).
       if (lane == 0) {
+        if (p.c_row_prefetch && !no_c) tma_prefetch_l2_2d(&tm_cpf, col0, row0);
         bulk_wait_group_read<0>();
 #pragma unroll
         for (int c = 0; c < Cfg::PRE; ++c) {
