@@ -49,7 +49,7 @@ struct PeerMaps {
 struct GemmParams {
   int M, N, K;
   int tiles_m, tiles_n, num_tiles;  // tiles of (128*CG) x BN
-  int k_blocks;                     // ceil(K / 64)
+  int k_blocks;                     // ceil(K / BK): smem ring stages per tile
   int kb_per_chunk;                 // k-blocks accumulated in TMEM before promotion to registers
   int k_chunks;                     // ceil(k_blocks / kb_per_chunk)
   int group_m;                      // raster group height in tiles
@@ -73,7 +73,8 @@ struct GemmParams {
   int epi_pace;                     // 1: spread each tile's C_in/C_out traffic over half a K-chunk
                                     // interval instead of a burst synchronised across all SMs
   unsigned long long* trace;        // DIAGNOSTIC ONLY (null normally): per-tile globaltimer stamps
-                                    // of CTA 0 (MMA start/end, epilogue drain/store), 8 per tile
+                                    // of CTA 0 (MMA start/end + SM cycles, epilogue drain/store),
+                                    // 8 per tile; row 62 = kernel entry/setup/exit
   int l2_hints;                     // 1: TMA loads/stores carry L2 eviction-priority hints
                                     // (A evict_last: re-read by the next wave of tiles;
                                     //  C evict_first: streamed once)
@@ -120,7 +121,7 @@ struct KCfg {
   static constexpr int NBAR = 2 * STAGES + 4 + EPI_WARPS * EPI_SLOTS;
   static constexpr int SMEM_BYTES = 1024 + OFF_BAR + NBAR * 8 + 16;
   static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of dynamic shared memory");
-  static constexpr int THREADS = 352;                 // 11 warps x <= 184 registers fit 64K
+  static constexpr int THREADS = 352;                 // 11 warps: <= 3 per SMSP x 168 registers
   static constexpr int W_PRODUCER = 8, W_MMA = 9, W_ALLOC = 10;
 };
 
