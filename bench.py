@@ -525,6 +525,7 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()   # rank 0 may still be on its CPU parity check
         dist.destroy_process_group()
     return 0
 
