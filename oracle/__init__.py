@@ -52,6 +52,8 @@ def _load():
         lib.oracle_f16_to_f64.argtypes = [ctypes.c_uint16]
         lib.oracle_f64_to_f16_rne.restype = ctypes.c_uint16
         lib.oracle_f64_to_f16_rne.argtypes = [ctypes.c_double]
+        lib.oracle_bf16_to_f64.restype = ctypes.c_double
+        lib.oracle_bf16_to_f64.argtypes = [ctypes.c_uint16]
         lib.oracle_num_threads.restype = ctypes.c_int
         lib.oracle_num_threads.argtypes = []
         i64 = ctypes.c_int64
@@ -59,6 +61,10 @@ def _load():
         lib.oracle_gemm_f16.restype = ctypes.c_int
         lib.oracle_gemm_f16.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64,
                                         ctypes.c_int, vp, i64, vp, vp]
+        ci = ctypes.c_int
+        lib.oracle_gemm_ex.restype = ci
+        lib.oracle_gemm_ex.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64,
+                                       ci, ci, ci, vp, ci, vp, i64, vp, vp]
         _lib = lib
     return _lib
 
@@ -75,6 +81,10 @@ def f64_to_f16_bits(x: float) -> int:
     return int(_load().oracle_f64_to_f16_rne(float(x)))
 
 
+def bf16_to_f64(bits: int) -> float:
+    return float(_load().oracle_bf16_to_f64(int(bits) & 0xFFFF))
+
+
 def _as_bits16(a: np.ndarray) -> np.ndarray:
     if a.dtype == np.float16:
         return a.view(np.uint16)
@@ -88,12 +98,13 @@ def _ptr(a: np.ndarray) -> int:
 
 
 def gemm(A: np.ndarray, B: np.ndarray, C_in: np.ndarray, acc: int | None = None,
-         rows=None):
-    """Oracle C_out = C_in + A.B over the given rows.
+         rows=None, in_type: int = 0, beta: int = 1, bias=None, relu: bool = False):
+    """Oracle C_out = epi(beta * C_in + A.B + bias) (NEXT #4 extensions).
 
-    A: (M, K) float16 (row stride may exceed K), B: (K, N) float16,
-    C_in: (M, N) float32 (F32 mode) or float16 (F16 mode).
-    rows: optional sequence of row indices; default all rows.
+    A: (M, K) float16 (or uint16 bfloat16 bits with in_type=1; row stride may
+    exceed K), B: (K, N) likewise, C_in: (M, N) float32 (F32 mode) or float16
+    (F16 mode).  rows: optional row indices (default all).  beta: 1 or 0 (C_in
+    ignored).  bias: optional (N,) float32.  relu: apply max(x, 0) (NaN kept).
     Returns (C_exact float64 (nrows, N), C_round (nrows, N) in C_in's dtype).
     """
     lib = _load()
@@ -123,13 +134,18 @@ def gemm(A: np.ndarray, B: np.ndarray, C_in: np.ndarray, acc: int | None = None,
     else:
         rows_arr = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
         nrows = rows_arr.shape[0]
+    bias_arr = None if bias is None else np.ascontiguousarray(np.asarray(bias, dtype=np.float32))
+    if bias_arr is not None and bias_arr.shape != (N,):
+        raise ValueError("bias must have N elements")
     C_exact = np.empty((nrows, N), dtype=np.float64)
     C_round = np.empty((nrows, N), dtype=want)
-    st = lib.oracle_gemm_f16(M, N, K, _ptr(Ab), lda, _ptr(Bb), ldb, _ptr(C_in), ldc,
-                             int(acc), None if rows_arr is None else _ptr(rows_arr),
-                             nrows, _ptr(C_exact), _ptr(C_round))
+    st = lib.oracle_gemm_ex(M, N, K, _ptr(Ab), lda, _ptr(Bb), ldb, _ptr(C_in), ldc,
+                            int(acc), int(in_type), int(beta),
+                            None if bias_arr is None else _ptr(bias_arr), int(bool(relu)),
+                            None if rows_arr is None else _ptr(rows_arr),
+                            nrows, _ptr(C_exact), _ptr(C_round))
     if st != 0:
-        raise ValueError(f"oracle_gemm_f16 rejected its arguments (status {st})")
+        raise ValueError(f"oracle_gemm_ex rejected its arguments (status {st})")
     return C_exact, C_round
 
 

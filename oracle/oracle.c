@@ -100,6 +100,26 @@ uint16_t oracle_f64_to_f16_rne(double x)
     return (uint16_t)(sign | (e << 10) | f);
 }
 
+/* bfloat16 -> double, exact: bfloat16 is the top half of an IEEE binary32
+ * (1 sign bit, 8 exponent bits with bias 127, 7 fraction bits).  Decoded from
+ * the fields, not by reinterpreting memory.  PAPER.md Sec. 2.3 P:272-275 lists
+ * BF16 among the tensor-core input formats. */
+double oracle_bf16_to_f64(uint16_t h)
+{
+    int sign = (h >> 15) & 1;
+    int e = (h >> 7) & 0xff;
+    int f = h & 0x7f;
+    double v;
+    if (e == 0) {
+        v = ldexp((double)f, -133);                 /* subnormal: f * 2^(1-127-7) */
+    } else if (e == 255) {
+        v = (f == 0) ? INFINITY : NAN;
+    } else {
+        v = ldexp((double)(f | 0x80), e - 134);     /* (1.f) * 2^(e-127), f has 7 bits */
+    }
+    return sign ? -v : v;
+}
+
 /* acc_type: 0 = F32 (C is float), 1 = F16 (C is binary16 bits). */
 static double load_c(const void* C, int64_t idx, int acc_type)
 {
@@ -120,6 +140,24 @@ static double load_c(const void* C, int64_t idx, int acc_type)
  * Returns 0, or -1 on an invalid argument (negative extent, short ld,
  * out-of-range row index).
  */
+/*
+ * oracle_gemm_ex: the fused-epilogue generalisation (the
+ * paper's motivation for fusion):
+ *     x_ij = beta * C_in[i][j] + sum_k A[i][k] * B[k][j] + bias[j]
+ *     out_ij = relu ? (x_ij > 0 ? x_ij : (x_ij is NaN ? x_ij : 0)) : x_ij
+ * evaluated in IEEE double (C_in first, then k ascending, then the bias), then
+ * rounded once to the output type.  in_type: 0 = binary16 A/B, 1 = bfloat16.
+ * beta: 0 or 1 (beta = 0 ignores C_in, which is then not read).  bias: NULL or
+ * N floats.  With in_type 0, beta 1, no bias, no relu this is oracle_gemm_f16.
+ */
+int oracle_gemm_ex(int64_t M, int64_t N, int64_t K,
+                   const uint16_t* A, int64_t lda,
+                   const uint16_t* B, int64_t ldb,
+                   const void* C_in, int64_t ldc,
+                   int acc_type, int in_type, int beta, const float* bias, int relu,
+                   const int64_t* rows, int64_t nrows,
+                   double* C_exact, void* C_round);
+
 int oracle_gemm_f16(int64_t M, int64_t N, int64_t K,
                     const uint16_t* A, int64_t lda,
                     const uint16_t* B, int64_t ldb,
@@ -128,6 +166,21 @@ int oracle_gemm_f16(int64_t M, int64_t N, int64_t K,
                     const int64_t* rows, int64_t nrows,
                     double* C_exact, void* C_round)
 {
+    return oracle_gemm_ex(M, N, K, A, lda, B, ldb, C_in, ldc, acc_type, 0, 1, NULL, 0, rows, nrows,
+                          C_exact, C_round);
+}
+
+int oracle_gemm_ex(int64_t M, int64_t N, int64_t K,
+                   const uint16_t* A, int64_t lda,
+                   const uint16_t* B, int64_t ldb,
+                   const void* C_in, int64_t ldc,
+                   int acc_type, int in_type, int beta, const float* bias, int relu,
+                   const int64_t* rows, int64_t nrows,
+                   double* C_exact, void* C_round)
+{
+    if (in_type != 0 && in_type != 1) return -1;
+    if (beta != 0 && beta != 1) return -1;
+    double (*decode)(uint16_t) = in_type == 0 ? oracle_f16_to_f64 : oracle_bf16_to_f64;
     if (M < 0 || N < 0 || K < 0) return -1;
     if (acc_type != 0 && acc_type != 1) return -1;
     if (K > 0 && lda < K) return -1;
@@ -142,7 +195,7 @@ int oracle_gemm_f16(int64_t M, int64_t N, int64_t K,
     if (!Bd) return -2;
     for (int64_t k = 0; k < K; ++k)
         for (int64_t j = 0; j < N; ++j)
-            Bd[k * N + j] = oracle_f16_to_f64(B[k * ldb + j]);
+            Bd[k * N + j] = decode(B[k * ldb + j]);
 
     int status = 0;
 #pragma omp parallel
@@ -156,14 +209,19 @@ int oracle_gemm_f16(int64_t M, int64_t N, int64_t K,
         for (int64_t r = 0; r < nrows; ++r) {
             if (!acc) continue;
             int64_t i = rows ? rows[r] : r;
-            /* x_ij starts at C_in[i][j] (C = AB + C) */
-            for (int64_t j = 0; j < N; ++j) acc[j] = load_c(C_in, i * ldc + j, acc_type);
+            /* x_ij starts at C_in[i][j] (C = AB + C), or at 0 when beta = 0 */
+            for (int64_t j = 0; j < N; ++j) acc[j] = beta ? load_c(C_in, i * ldc + j, acc_type) : 0.0;
             /* k ascending: x_ij += A[i][k] * B[k][j]  (lst:naive-affine) */
             for (int64_t k = 0; k < K; ++k) {
-                double a = oracle_f16_to_f64(A[i * lda + k]);
+                double a = decode(A[i * lda + k]);
                 const double* brow = Bd + k * N;
                 for (int64_t j = 0; j < N; ++j) acc[j] += a * brow[j];
             }
+            if (bias)   /* + bias[j], broadcast over rows */
+                for (int64_t j = 0; j < N; ++j) acc[j] += (double)bias[j];
+            if (relu)   /* max(x, 0), NaN propagates */
+                for (int64_t j = 0; j < N; ++j)
+                    if (!(acc[j] > 0.0) && !isnan(acc[j])) acc[j] = 0.0;
             if (C_exact) memcpy(C_exact + r * N, acc, (size_t)N * sizeof(double));
             if (C_round) {
                 if (acc_type == 0) {

@@ -69,6 +69,21 @@ def uniform_f16(seed: int, matrix_id: int, rows: int, cols: int, **kw) -> np.nda
     return uniform_f32(seed, matrix_id, rows, cols, **kw).astype(np.float16)
 
 
+def to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    """float32 -> bfloat16 bit patterns (uint16), round to nearest even (NaN kept quiet)."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    with np.errstate(over="ignore"):
+        r = (b + np.uint32(0x7FFF) + ((b >> np.uint32(16)) & np.uint32(1))) >> np.uint32(16)
+    nan = (b & np.uint32(0x7FFFFFFF)) > np.uint32(0x7F800000)
+    r = np.where(nan, (b >> np.uint32(16)) | np.uint32(0x40), r)
+    return r.astype(np.uint16)
+
+
+def uniform_bf16(seed: int, matrix_id: int, rows: int, cols: int, **kw) -> np.ndarray:
+    """uniform_f32 rounded to bfloat16, returned as uint16 bit patterns."""
+    return to_bf16_bits(uniform_f32(seed, matrix_id, rows, cols, **kw))
+
+
 def problem(M: int, N: int, K: int, acc: str = "f32", seed: int = 0):
     """(A (M,K) f16, B (K,N) f16, C_in (M,N) f32|f16) for one seeded problem."""
     A = uniform_f16(seed, MATRIX_A, M, K)
@@ -79,6 +94,14 @@ def problem(M: int, N: int, K: int, acc: str = "f32", seed: int = 0):
         C = uniform_f16(seed, MATRIX_C, M, N)
     else:
         raise ValueError(acc)
+    return A, B, C
+
+
+def problem_bf16(M: int, N: int, K: int, acc: str = "f32", seed: int = 0):
+    """(A bf16 bits (M,K) uint16, B bf16 bits (K,N) uint16, C_in f32|f16) -- BF16 inputs."""
+    A = uniform_bf16(seed, MATRIX_A, M, K)
+    B = uniform_bf16(seed, MATRIX_B, K, N)
+    C = uniform_f32(seed, MATRIX_C, M, N) if acc == "f32" else uniform_f16(seed, MATRIX_C, M, N)
     return A, B, C
 
 

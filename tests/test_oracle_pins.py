@@ -250,3 +250,75 @@ def test_invalid_arguments_rejected():
         oracle.gemm(A, B, C, rows=[4])
     with pytest.raises(ValueError):
         oracle.gemm(A, B[:3], C)
+
+
+# ---------------------------------------------------------------- NEXT #4 extensions
+# (BF16 inputs P:272-275, fused bias / ReLU P:87-89, beta = 0)
+
+def test_bf16_decoder_all_patterns():
+    import torch
+    bits = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    ref = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).to(torch.float64).numpy()
+    got = np.array([oracle.bf16_to_f64(int(b)) for b in bits])
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(got), nan)
+    assert np.array_equal(got[~nan], ref[~nan])
+
+
+def _bf16_val(bits):
+    import torch
+    return torch.from_numpy(np.asarray(bits).view(np.int16)).view(torch.bfloat16).to(torch.float64).numpy()
+
+
+def test_bf16_exact_rationals():
+    rng = np.random.default_rng(8)
+    for trial in range(20):
+        M, N, K = (int(x) for x in rng.integers(1, 12, size=3))
+        A, B, C = synth.problem_bf16(M, N, K, "f32", seed=trial % 5)
+        ex, _ = oracle.gemm(A, B, C, in_type=1)
+        Av, Bv = _bf16_val(A), _bf16_val(B)
+        u = 2.0 ** -53
+        gamma = (K + 1) * u / (1 - (K + 1) * u)
+        for i in range(M):
+            for j in range(N):
+                e = Fraction(float(C[i, j])) + sum(Fraction(float(Av[i, k])) * Fraction(float(Bv[k, j])) for k in range(K))
+                bound = gamma * (abs(float(C[i, j])) + sum(abs(Av[i, k] * Bv[k, j]) for k in range(K)))
+                assert abs(Fraction(ex[i, j]) - e) <= Fraction(bound)
+
+
+def test_beta0_ignores_C_in():
+    K, N = 80, 56
+    _, B, _ = synth.problem(K, N, K, "f32", seed=2)
+    C_nan = np.full((K, N), np.nan, np.float32)
+    ex, rd = oracle.gemm(np.eye(K, dtype=np.float16), B, C_nan, beta=0)
+    assert np.array_equal(ex, B.astype(np.float64)) and np.array_equal(rd, B.astype(np.float32))
+
+
+def test_bias_broadcast_and_relu_closed_forms():
+    rng = np.random.default_rng(9)
+    M, N, K = 40, 33, 70
+    Ai = rng.integers(-2, 3, size=(M, K))
+    Bi = rng.integers(-2, 3, size=(K, N))
+    Ci = rng.integers(-60, 61, size=(M, N))
+    bias = rng.integers(-30, 31, size=N).astype(np.float32)
+    for relu in (False, True):
+        for beta in (0, 1):
+            ex, rd = oracle.gemm(Ai.astype(np.float16), Bi.astype(np.float16), Ci.astype(np.float32),
+                                 beta=beta, bias=bias, relu=relu)
+            want = (Ai @ Bi + beta * Ci + bias.astype(np.int64)[None, :]).astype(np.float64)
+            if relu:
+                want = np.maximum(want, 0.0)
+            assert np.array_equal(ex, want), (relu, beta)
+    # A = 0: out = relu(C_in + bias), per column
+    A0 = np.zeros((M, K), np.float16)
+    ex, _ = oracle.gemm(A0, Bi.astype(np.float16), Ci.astype(np.float32), bias=bias, relu=True)
+    assert np.array_equal(ex, np.maximum(Ci + bias[None, :].astype(np.int64), 0).astype(np.float64))
+
+
+def test_relu_keeps_nan():
+    A = np.array([[np.nan, 1.0]], np.float16)
+    B = np.array([[1.0], [1.0]], np.float16)
+    ex, rd = oracle.gemm(A, B, np.zeros((1, 1), np.float32), relu=True)
+    assert np.isnan(ex[0, 0]) and np.isnan(rd[0, 0])
+    ex, _ = oracle.gemm(np.array([[-3.0]], np.float16), np.array([[2.0]], np.float16), np.zeros((1, 1), np.float32), relu=True)
+    assert ex[0, 0] == 0.0

@@ -37,3 +37,13 @@ def test_sample_rows_cover_tile_edges():
     for t in range(0, 1000, 128):
         assert t in rows and min(999, t + 127) in rows
     assert rows.min() >= 0 and rows.max() < 1000
+
+
+def test_bf16_rounding_matches_torch():
+    import torch
+    rng = np.random.default_rng(3)
+    x = np.concatenate([rng.standard_normal(20000).astype(np.float32) * np.float32(10.0) ** rng.integers(-30, 30, 20000).astype(np.float32),
+                        np.array([0.0, -0.0, 1.0, 65504.0, 3.0e38, np.inf, -np.inf, 1e-40], np.float32)])
+    ours = synth.to_bf16_bits(x)
+    ref = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(ours, ref)
