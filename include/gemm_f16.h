@@ -43,6 +43,12 @@ typedef enum {
   GEMM_ACC_F16 = 1  /* C is IEEE binary16; F16 in/out, see R3     */
 } gemm_acc_t;
 
+/* Input element type of A and B (gemm_options_t.in_type). */
+typedef enum {
+  GEMM_IN_F16 = 0,  /* IEEE binary16 (the paper's evaluated inputs) */
+  GEMM_IN_BF16 = 1  /* bfloat16 (same tensor-core rate)                      */
+} gemm_in_t;
+
 typedef enum {
   GEMM_OK = 0,
   GEMM_ERR_INVALID_VALUE = 1,      /* negative extent, short leading dim, NULL with work, bad mode/option */
@@ -88,6 +94,12 @@ typedef struct {
                     /* waiting for an accumulator; -1: plain polling                     */
   int c_row_prefetch; /* 0: default; 1: at tile start each epilogue warp L2-prefetches its */
                     /* whole C_in region in full rows; -1: off                           */
+  /* Fused epilogue (the paper's fusion motivation):       */
+  /*   C <- relu?( beta * C_in + A.B + bias[j] ), one rounding to C's type                */
+  int in_type;      /* gemm_in_t: GEMM_IN_F16 (default) or GEMM_IN_BF16 for A and B       */
+  int beta0;        /* 0: C += A.B (default); 1: C = A.B (C_in not read)                  */
+  int relu;         /* 1: max(x, 0) applied before rounding (NaN propagates)              */
+  const void* bias; /* NULL, or device float[N] added to every row (16-byte aligned)      */
   void* trace;      /* DIAGNOSTIC ONLY, normally NULL: device buffer of 512 uint64 that   */
                     /* receives per-tile globaltimer stamps of CTA 0                      */
 } gemm_options_t;

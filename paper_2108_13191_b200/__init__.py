@@ -56,7 +56,8 @@ class _Options(ctypes.Structure):
                 ("l2_hints", ctypes.c_int), ("debug_flags", ctypes.c_int), ("promote_k", ctypes.c_int),
                 ("epi_pace", ctypes.c_int), ("ring_stages", ctypes.c_int), ("acc_bufs", ctypes.c_int),
                 ("k_serpentine", ctypes.c_int), ("wait_hint_ns", ctypes.c_int),
-                ("c_row_prefetch", ctypes.c_int), ("trace", ctypes.c_void_p)]
+                ("c_row_prefetch", ctypes.c_int), ("in_type", ctypes.c_int), ("beta0", ctypes.c_int),
+                ("relu", ctypes.c_int), ("bias", ctypes.c_void_p), ("trace", ctypes.c_void_p)]
 
 
 _lib = None
@@ -141,20 +142,28 @@ def _acc_of(C):
 def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int = 0, l2_hints: int = 0,
              debug_flags: int = 0, promote_k: int = 0, epi_pace: int = 0, ring_stages: int = 0,
              acc_bufs: int = 0, k_serpentine: int = 0, wait_hint_ns: int = 0, c_row_prefetch: int = 0,
-             trace=None):
+             beta: int = 1, bias=None, relu: bool = False, trace=None):
     """In place: C += A @ B on the GPU (enqueued on `stream`, default: torch's current).
 
-    A: (M, K) torch.float16 CUDA, B: (K, N) torch.float16 CUDA, C: (M, N) float32 or
-    float16 CUDA; all row-major with unit column stride (row strides = leading dims).
-    config: a name in CONFIGS or its id (0 = auto).  Raises GemmError on a non-zero status.
+    A: (M, K) torch.float16 or torch.bfloat16 CUDA, B: (K, N) of the same dtype,
+    C: (M, N) float32 or float16 CUDA; all row-major with unit column stride (row
+    strides = leading dims).  Fused epilogue: C <- relu?(beta * C + A @ B + bias),
+    beta in {1, 0}, bias an (N,) float32 CUDA tensor.  config: a name in CONFIGS or
+    its id (0 = auto).  Raises GemmError on a non-zero status.
     """
     import torch
     lib = load_library()
     for name, t in (("A", A), ("B", B), ("C", C)):
         if not t.is_cuda:
             raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
-    if A.dtype != torch.float16 or B.dtype != torch.float16:
-        raise TypeError("A and B must be torch.float16")
+    if A.dtype not in (torch.float16, torch.bfloat16) or B.dtype != A.dtype:
+        raise TypeError("A and B must both be torch.float16 or both torch.bfloat16")
+    in_type = 1 if A.dtype == torch.bfloat16 else 0
+    if beta not in (0, 1):
+        raise ValueError("beta must be 1 (C += A.B) or 0 (C = A.B)")
+    if bias is not None and (bias.dtype != torch.float32 or bias.dim() != 1 or bias.numel() != B.shape[1]
+                             or not bias.is_cuda or bias.stride(0) != 1):
+        raise ValueError("bias must be a contiguous float32 CUDA vector of N elements")
     if A.device != C.device or B.device != C.device:
         raise ValueError("A, B and C must be on the same CUDA device")
     acc = _acc_of(C)
@@ -172,13 +181,15 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
         sh = _stream_handle(stream, dev)
         if (cfg == 0 and not max_clusters and not group_m and not l2_hints and not debug_flags and not promote_k
                 and not epi_pace and not ring_stages and not acc_bufs and not k_serpentine and not wait_hint_ns
-                and not c_row_prefetch and trace is None):
+                and not c_row_prefetch and trace is None and in_type == 0 and beta == 1 and bias is None
+                and not relu):
             st = lib.gemm_f16(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
                               C.data_ptr(), _ld(C, "C"), acc, sh)
         else:
             opts = _Options(cfg, int(max_clusters), int(group_m), int(l2_hints), int(debug_flags), int(promote_k),
                             int(epi_pace), int(ring_stages), int(acc_bufs), int(k_serpentine),
-                            int(wait_hint_ns), int(c_row_prefetch),
+                            int(wait_hint_ns), int(c_row_prefetch), in_type, 1 - int(beta), int(bool(relu)),
+                            None if bias is None else ctypes.c_void_p(bias.data_ptr()),
                             None if trace is None else ctypes.c_void_p(trace.data_ptr()))
             st = lib.gemm_f16_ex(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
                                  C.data_ptr(), _ld(C, "C"), acc, sh, ctypes.byref(opts))

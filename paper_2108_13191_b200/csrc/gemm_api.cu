@@ -309,10 +309,16 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const ConfigDesc& cd = cfg == GEMM_CFG_COUNT ? kGatherConfig : kConfigs[cfg];
   const int a = acc_type;
 
+  const int in_type = opts ? opts->in_type : GEMM_IN_F16;
+  if (in_type != GEMM_IN_F16 && in_type != GEMM_IN_BF16) return GEMM_ERR_INVALID_VALUE;
+  const CUtensorMapDataType in_dt =
+      in_type == GEMM_IN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const float* bias = opts ? static_cast<const float*>(opts->bias) : nullptr;
+  if (bias && !aligned16(bias)) return GEMM_ERR_MISALIGNED;
   CUtensorMap tm_a, tm_b, tm_c;
   const bool ok =
-      encode_2d(&tm_a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, A, M, K, lda, 64, 128, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
-      encode_2d(&tm_b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, B, K, N, ldb, 64, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
+      encode_2d(&tm_a, in_dt, 2, A, M, K, lda, 64, 128, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
+      encode_2d(&tm_b, in_dt, 2, B, K, N, ldb, 64, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
       encode_2d(&tm_c, acc_type == GEMM_ACC_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                 acc_type == GEMM_ACC_F32 ? 4 : 2, C, M, N, ldc, static_cast<uint32_t>(cd.c_box_cols[a]), 32,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -363,6 +369,10 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (hints < -1 || hints > 1) return GEMM_ERR_INVALID_VALUE;
   p.l2_hints = hints == 0 ? kDefaultL2Hints : (hints > 0 ? 1 : 0);
   p.debug_flags = opts ? opts->debug_flags : 0;
+  p.in_bf16 = in_type == GEMM_IN_BF16;
+  p.beta0 = (opts && opts->beta0) ? 1 : 0;
+  p.relu = (opts && opts->relu) ? 1 : 0;
+  p.bias = bias;
   p.trace = opts ? static_cast<unsigned long long*>(opts->trace) : nullptr;
   const int pace = opts ? opts->epi_pace : 0;
   if (pace < -1 || pace > 1) return GEMM_ERR_INVALID_VALUE;

@@ -75,6 +75,11 @@ struct GemmParams {
   unsigned long long* trace;        // DIAGNOSTIC ONLY (null normally): per-tile globaltimer stamps
                                     // of CTA 0 (MMA start/end + SM cycles, epilogue drain/store),
                                     // 8 per tile; row 62 = kernel entry/setup/exit
+  // fused epilogue: out = relu?(beta * C_in + A.B + bias[col])
+  int in_bf16;                      // 1: A and B are bfloat16 (idesc a/b_format = BF16)
+  int beta0;                        // 1: C_in is not read (beta = 0)
+  int relu;                         // 1: max(x, 0) with NaN propagated, before the rounding
+  const float* bias;                // null, or N floats added per column (16-byte aligned)
   int l2_hints;                     // 1: TMA loads/stores carry L2 eviction-priority hints
                                     // (A evict_last: re-read by the next wave of tiles;
                                     //  C evict_first: streamed once)
@@ -167,6 +172,17 @@ template <int RB>
 __device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t j) {
   return r * RB + ((j ^ (((r * RB) >> 7) & (RB / 16 - 1))) << 4);
 }
+
+__device__ __forceinline__ float4 load_bias4(const float* bias, int col, int n) {
+  if (col + 3 < n) return __ldg(reinterpret_cast<const float4*>(bias + col));
+  float4 r;
+  r.x = col < n ? __ldg(bias + col) : 0.f;
+  r.y = col + 1 < n ? __ldg(bias + col + 1) : 0.f;
+  r.z = col + 2 < n ? __ldg(bias + col + 2) : 0.f;
+  r.w = 0.f;
+  return r;
+}
+__device__ __forceinline__ float relu_keep_nan(float x) { return (x > 0.f || x != x) ? x : 0.f; }
 
 template <class Cfg>
 __global__ void __launch_bounds__(352, 1)
@@ -276,7 +292,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   } else if (warp == Cfg::W_MMA) {
     // ===================== MMA issuer (pair leader) =====================
     if (rank == 0 && lane == 0) {
-      constexpr uint32_t idesc = idesc_f16_f32acc<BM * CG, BN>();
+      const uint32_t idesc = idesc_f16_f32acc<BM * CG, BN>() | (p.in_bf16 ? ((1u << 7) | (1u << 10)) : 0u);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -335,6 +351,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     const uint32_t acce_leader = (CG == 2) ? mapa_shared(acce_bar, 0) : acce_bar;
     const uint64_t pol_c = p.l2_hints ? policy_evict_first() : policy_evict_normal();
     const bool no_c = (p.debug_flags & 2) != 0;
+    const bool load_c = !no_c && !p.beta0;   // C_in traffic (beta = 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t slot_phase = 0;  // bit s = parity to wait for on slot s
@@ -352,12 +369,12 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       // now, so its latency hides under this tile's MMAs (the slots were freed by
       // the previous tile's stores).
       if (lane == 0) {
-        if (p.c_row_prefetch && !no_c) tma_prefetch_l2_2d(&tm_cpf, col0, row0);
+        if (p.c_row_prefetch && load_c) tma_prefetch_l2_2d(&tm_cpf, col0, row0);
         bulk_wait_group_read<0>();
 #pragma unroll
         for (int c = 0; c < Cfg::PRE; ++c) {
           const uint32_t sbar = ebar0 + 8 * c;
-          if (!no_c) {
+          if (load_c) {
             mbar_arrive_expect_tx(sbar, 32 * Cfg::RB);
             tma_load_2d_hint(ebuf0 + c * Cfg::EPI_BUF, &tm_c, col0 + c * Cfg::CW, row0, sbar, pol_c);
           } else {
@@ -369,7 +386,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       const uint32_t t_lane = tmem_base + ((q * 32u) << 16) + hcol;
 #pragma unroll 1
       for (int ch = 0; ch < p.k_chunks; ++ch) {
-        if (Cfg::PRE < Cfg::NOUT && ch == p.k_chunks - 1 && lane == 0 && !no_c) {
+        if (Cfg::PRE < Cfg::NOUT && ch == p.k_chunks - 1 && lane == 0 && load_c) {
           // the remaining C_in chunks are needed right after this (last) K chunk:
           // pull them into L2 now, one chunk ahead, so they are neither evicted by
           // a whole tile of operand traffic nor fetched from HBM in a burst.
@@ -432,19 +449,36 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         for (int j = 0; j < Cfg::RB / 16; ++j) {
           const uint32_t addr = sbuf + swz<Cfg::RB>(lane, static_cast<uint32_t>(j));
           const float* a = &racc[c * Cfg::CW + j * (16 / Cfg::ESIZE)];
+          constexpr int EPU = 16 / Cfg::ESIZE;      // output elements per 16-byte unit
+          float o[EPU];
           if constexpr (!Cfg::OUT_F16) {
-            const float4 ci = lds128(addr);
-            const float o0 = ci.x + a[0], o1 = ci.y + a[1], o2 = ci.z + a[2], o3 = ci.w + a[3];
-            sts128(addr, o0, o1, o2, o3);
+            float4 ci = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!p.beta0) ci = lds128(addr);
+            o[0] = ci.x + a[0]; o[1] = ci.y + a[1]; o[2] = ci.z + a[2]; o[3] = ci.w + a[3];
           } else {
-            const uint4 ci = lds128u(addr);
+            uint4 ci = make_uint4(0u, 0u, 0u, 0u);
+            if (!p.beta0) ci = lds128u(addr);
             const float2 c0 = f16x2_to_f32(ci.x), c1 = f16x2_to_f32(ci.y);
             const float2 c2 = f16x2_to_f32(ci.z), c3 = f16x2_to_f32(ci.w);
-            const uint32_t o0 = cvt_f16x2_rn(c0.x + a[0], c0.y + a[1]);
-            const uint32_t o1 = cvt_f16x2_rn(c1.x + a[2], c1.y + a[3]);
-            const uint32_t o2 = cvt_f16x2_rn(c2.x + a[4], c2.y + a[5]);
-            const uint32_t o3 = cvt_f16x2_rn(c3.x + a[6], c3.y + a[7]);
-            sts128u(addr, o0, o1, o2, o3);
+            o[0] = c0.x + a[0]; o[1] = c0.y + a[1]; o[2] = c1.x + a[2]; o[3] = c1.y + a[3];
+            o[4] = c2.x + a[4]; o[5] = c2.y + a[5]; o[6] = c3.x + a[6]; o[7] = c3.y + a[7];
+          }
+          if (p.bias != nullptr) {
+#pragma unroll
+            for (int h = 0; h < EPU / 4; ++h) {
+              const float4 bb = load_bias4(p.bias, ccol + EPU * j + 4 * h, p.N);
+              o[4 * h + 0] += bb.x; o[4 * h + 1] += bb.y; o[4 * h + 2] += bb.z; o[4 * h + 3] += bb.w;
+            }
+          }
+          if (p.relu) {
+#pragma unroll
+            for (int e = 0; e < EPU; ++e) o[e] = relu_keep_nan(o[e]);
+          }
+          if constexpr (!Cfg::OUT_F16) {
+            sts128(addr, o[0], o[1], o[2], o[3]);
+          } else {
+            sts128u(addr, cvt_f16x2_rn(o[0], o[1]), cvt_f16x2_rn(o[2], o[3]), cvt_f16x2_rn(o[4], o[5]),
+                    cvt_f16x2_rn(o[6], o[7]));
           }
         }
         if (!manual && !no_c) {
@@ -486,7 +520,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         if (c + Cfg::EPI_SLOTS < Cfg::NOUT && lane == 0) {
           // refill this slot with chunk c + SLOTS once its store has read it
           bulk_wait_group_read<0>();
-          if (!no_c) {
+          if (load_c) {
             mbar_arrive_expect_tx(sbar, 32 * Cfg::RB);
             tma_load_2d_hint(sbuf, &tm_c, ccol + Cfg::EPI_SLOTS * Cfg::CW, row0, sbar, pol_c);
           } else {

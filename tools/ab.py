@@ -12,9 +12,14 @@ A = torch.from_numpy(synth.uniform_f16(0, 0, M, K)).cuda()
 B = torch.from_numpy(synth.uniform_f16(0, 1, K, N)).cuda()
 Cs = {"f32": torch.from_numpy(synth.uniform_f32(0, 2, M, N)).cuda(), "f16": torch.from_numpy(synth.uniform_f16(0, 2, M, N)).cuda()}
 res = {i: [] for i in range(len(variants))}
+Ab, Bb = A.bfloat16(), B.bfloat16()
+bias_vec = torch.from_numpy(synth.uniform_f32(7, 3, 1, N)[0]).cuda()
 def run(v):
-    kw = {k: x for k, x in v.items() if k != "mode"}
-    g.gemm_f16(A, B, Cs[v.get("mode", "f32")], **kw)
+    kw = {k: x for k, x in v.items() if k not in ("mode", "bf16", "bias")}
+    if v.get("bias"):
+        kw["bias"] = bias_vec
+    a, b = (Ab, Bb) if v.get("bf16") else (A, B)
+    g.gemm_f16(a, b, Cs[v.get("mode", "f32")], **kw)
 for v in variants:
     for _ in range(3): run(v)
 torch.cuda.synchronize()
