@@ -93,7 +93,8 @@ typedef struct {
   int wait_hint_ns; /* 0: default; >0: suspend-time hint (ns) for the epilogue warps      */
                     /* waiting for an accumulator; -1: plain polling                     */
   int c_row_prefetch; /* 0: default; 1: at tile start each epilogue warp L2-prefetches its */
-                    /* whole C_in region in full rows; -1: off                           */
+                    /* whole C_in region in full rows; 2: ... the NEXT tile's region     */
+                    /* (one tile ahead); -1: off                                         */
   /* Fused epilogue (the paper's fusion motivation):       */
   /*   C <- relu?( beta * C_in + A.B + bias[j] ), one rounding to C's type                */
   int in_type;      /* gemm_in_t: GEMM_IN_F16 (default) or GEMM_IN_BF16 for A and B       */

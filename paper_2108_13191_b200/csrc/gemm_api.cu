@@ -390,8 +390,8 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (wh < -1) return GEMM_ERR_INVALID_VALUE;
   p.wait_hint_ns = wh == 0 ? kDefaultWaitHintNs : (wh < 0 ? 0u : static_cast<unsigned>(wh));
   const int crp = opts ? opts->c_row_prefetch : 0;
-  if (crp < -1 || crp > 1) return GEMM_ERR_INVALID_VALUE;
-  p.c_row_prefetch = crp == 0 ? kDefaultCRowPrefetch : (crp > 0 ? 1 : 0);
+  if (crp < -1 || crp > 2) return GEMM_ERR_INVALID_VALUE;
+  p.c_row_prefetch = crp == 0 ? kDefaultCRowPrefetch : (crp > 0 ? crp : 0);
 
   // persistent grid: one cluster per resident slot; an explicit max_clusters may
   // also exceed the resident slots (a non-persistent launch, for ablation)

@@ -63,7 +63,8 @@ struct GemmParams {
   int debug_flags;                  // DIAGNOSTIC ONLY (wrong results): 1 = no operand TMA after
                                     // the ring is filled once per tile, 2 = no C_in/C_out traffic
   int c_row_prefetch;               // 1: at tile start, one L2 prefetch per epilogue warp of its
-                                    // whole C_in region (full 32 x CPW rows: long DRAM bursts)
+                                    // whole C_in region (full 32 x CPW rows: long DRAM bursts);
+                                    // 2: the producer prefetches the NEXT tile's C_in region
   unsigned wait_hint_ns;            // suspend-time hint for the epilogue's accumulator waits
                                     // (0 = plain polling); the producer/MMA always poll
   int k_serpentine;                 // 1: odd persistent iterations walk K backwards, so the next
@@ -256,6 +257,19 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         const int a_row = tm * BM * CG + static_cast<int>(rank) * BM;
         const int b_col = tn * BN + static_cast<int>(rank) * Cfg::BN_CTA;
         const bool backwards = p.k_serpentine && (it & 1);
+        if (p.c_row_prefetch == 2 && !p.beta0 && !(p.debug_flags & 2) && tile + nclusters < p.num_tiles) {
+          // C_in one tile ahead: this CTA's region of the NEXT tile streams into L2
+          // under this tile's MMAs, so the epilogue's slot loads hit L2 instead of
+          // all SMs fetching from HBM in a burst when their tiles end together
+          int ntm, ntn;
+          tile_coords(tile + nclusters, p, ntm, ntn);
+          const int crow = ntm * BM * CG + static_cast<int>(rank) * BM;
+#pragma unroll 1
+          for (int r = 0; r < BM; r += 32) {
+            tma_prefetch_l2_2d(&tm_cpf, ntn * BN, crow + r);
+            tma_prefetch_l2_2d(&tm_cpf, ntn * BN + BN / 2, crow + r);
+          }
+        }
         for (int kbi = 0; kbi < p.k_blocks; ++kbi) {
           const int kb = backwards ? p.k_blocks - 1 - kbi : kbi;
           mbar_wait(empty_bar + 8 * stage, phase ^ 1u);
