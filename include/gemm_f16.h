@@ -103,6 +103,10 @@ typedef struct {
   const void* bias; /* NULL, or device float[N] added to every row (16-byte aligned)      */
   void* trace;      /* DIAGNOSTIC ONLY, normally NULL: device buffer of 512 uint64 that   */
                     /* receives per-tile globaltimer stamps of CTA 0                      */
+  int accum_f16;    /* EXPERIMENT, 0 normally: 1 = the tensor core accumulates in binary16 */
+                    /* (instruction c_format F16: the paper's literal F16 accumulation,   */
+                    /* P:979-980; DESIGN R3/R16).  Partial sums are still promoted into   */
+                    /* F32 registers every promote_k (-1: one binary16 chain per tile)    */
 } gemm_options_t;
 
 /*

@@ -57,7 +57,8 @@ class _Options(ctypes.Structure):
                 ("epi_pace", ctypes.c_int), ("ring_stages", ctypes.c_int), ("acc_bufs", ctypes.c_int),
                 ("k_serpentine", ctypes.c_int), ("wait_hint_ns", ctypes.c_int),
                 ("c_row_prefetch", ctypes.c_int), ("in_type", ctypes.c_int), ("beta0", ctypes.c_int),
-                ("relu", ctypes.c_int), ("bias", ctypes.c_void_p), ("trace", ctypes.c_void_p)]
+                ("relu", ctypes.c_int), ("bias", ctypes.c_void_p), ("trace", ctypes.c_void_p),
+                ("accum_f16", ctypes.c_int)]
 
 
 _lib = None
@@ -142,14 +143,15 @@ def _acc_of(C):
 def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int = 0, l2_hints: int = 0,
              debug_flags: int = 0, promote_k: int = 0, epi_pace: int = 0, ring_stages: int = 0,
              acc_bufs: int = 0, k_serpentine: int = 0, wait_hint_ns: int = 0, c_row_prefetch: int = 0,
-             beta: int = 1, bias=None, relu: bool = False, trace=None):
+             beta: int = 1, bias=None, relu: bool = False, trace=None, accum_f16: bool = False):
     """In place: C += A @ B on the GPU (enqueued on `stream`, default: torch's current).
 
     A: (M, K) torch.float16 or torch.bfloat16 CUDA, B: (K, N) of the same dtype,
     C: (M, N) float32 or float16 CUDA; all row-major with unit column stride (row
     strides = leading dims).  Fused epilogue: C <- relu?(beta * C + A @ B + bias),
     beta in {1, 0}, bias an (N,) float32 CUDA tensor.  config: a name in CONFIGS or
-    its id (0 = auto).  Raises GemmError on a non-zero status.
+    its id (0 = auto).  accum_f16 (EXPERIMENT): the tensor core accumulates in
+    binary16 (DESIGN R16).  Raises GemmError on a non-zero status.
     """
     import torch
     lib = load_library()
@@ -182,7 +184,7 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
         if (cfg == 0 and not max_clusters and not group_m and not l2_hints and not debug_flags and not promote_k
                 and not epi_pace and not ring_stages and not acc_bufs and not k_serpentine and not wait_hint_ns
                 and not c_row_prefetch and trace is None and in_type == 0 and beta == 1 and bias is None
-                and not relu):
+                and not relu and not accum_f16):
             st = lib.gemm_f16(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
                               C.data_ptr(), _ld(C, "C"), acc, sh)
         else:
@@ -190,7 +192,7 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
                             int(epi_pace), int(ring_stages), int(acc_bufs), int(k_serpentine),
                             int(wait_hint_ns), int(c_row_prefetch), in_type, 1 - int(beta), int(bool(relu)),
                             None if bias is None else ctypes.c_void_p(bias.data_ptr()),
-                            None if trace is None else ctypes.c_void_p(trace.data_ptr()))
+                            None if trace is None else ctypes.c_void_p(trace.data_ptr()), int(bool(accum_f16)))
             st = lib.gemm_f16_ex(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
                                  C.data_ptr(), _ld(C, "C"), acc, sh, ctypes.byref(opts))
     finally:

@@ -372,6 +372,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   p.in_bf16 = in_type == GEMM_IN_BF16;
   p.beta0 = (opts && opts->beta0) ? 1 : 0;
   p.relu = (opts && opts->relu) ? 1 : 0;
+  p.accum_f16 = (opts && opts->accum_f16) ? 1 : 0;
   p.bias = bias;
   p.trace = opts ? static_cast<unsigned long long*>(opts->trace) : nullptr;
   const int pace = opts ? opts->epi_pace : 0;

@@ -81,6 +81,9 @@ struct GemmParams {
   int beta0;                        // 1: C_in is not read (beta = 0)
   int relu;                         // 1: max(x, 0) with NaN propagated, before the rounding
   const float* bias;                // null, or N floats added per column (16-byte aligned)
+  int accum_f16;                    // EXPERIMENT (SURVEY A3 "strict"): idesc c_format = F16, the
+                                    // tensor core accumulates in binary16; TMEM cells hold the
+                                    // F16 value in their low 16 bits
   int l2_hints;                     // 1: TMA loads/stores carry L2 eviction-priority hints
                                     // (A evict_last: re-read by the next wave of tiles;
                                     //  C evict_first: streamed once)
@@ -306,7 +309,8 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   } else if (warp == Cfg::W_MMA) {
     // ===================== MMA issuer (pair leader) =====================
     if (rank == 0 && lane == 0) {
-      const uint32_t idesc = idesc_f16_f32acc<BM * CG, BN>() | (p.in_bf16 ? ((1u << 7) | (1u << 10)) : 0u);
+      const uint32_t idesc = (idesc_f16_f32acc<BM * CG, BN>() & (p.accum_f16 ? ~(3u << 4) : ~0u)) |
+                             (p.in_bf16 ? ((1u << 7) | (1u << 10)) : 0u);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -422,6 +426,10 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           uint32_t v[32];
           tmem_ld_32x32b_x32(t_row + 32 * c, v);
           tmem_wait_ld();
+          if (p.accum_f16) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(f16x2_to_f32(v[j]).x);
+          }
           if (ch == 0) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) racc[32 * c + j] = __uint_as_float(v[j]);
