@@ -107,6 +107,9 @@ typedef struct {
                     /* (instruction c_format F16: the paper's literal F16 accumulation,   */
                     /* P:979-980; DESIGN R3/R16).  Partial sums are still promoted into   */
                     /* F32 registers every promote_k (-1: one binary16 chain per tile)    */
+  int pdl;          /* 0: default; 1: programmatic dependent launch (the kernel's prologue */
+                    /* overlaps the previous grid's tail in the stream; it waits for that  */
+                    /* grid before touching global memory); -1: off                        */
 } gemm_options_t;
 
 /*

@@ -26,6 +26,7 @@ constexpr int kDefaultEpiPace = 0;
 constexpr int kDefaultKSerpentine = 0;
 constexpr unsigned kDefaultWaitHintNs = 0;
 constexpr int kDefaultCRowPrefetch = 0;
+constexpr int kDefaultPdl = 1;   // profiles/r01/findings.md section 9
 
 thread_local int t_last_cuda_error = 0;
 thread_local int t_last_launches = 0;
@@ -114,7 +115,7 @@ void init_device(int dev) {
         e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.fn[a]),
                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
         cudaLaunchConfig_t lc = {};
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = 2;
         attr[0].val.clusterDim.y = 1;
@@ -402,7 +403,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   clusters = static_cast<int>(std::min<int64_t>(clusters, tiles));
 
   cudaLaunchConfig_t lc = {};
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   lc.gridDim = dim3(static_cast<unsigned>(clusters * cd.cta_group), 1, 1);
   lc.blockDim = dim3(static_cast<unsigned>(cd.threads), 1, 1);
   lc.dynamicSmemBytes = cd.smem[a];
@@ -412,9 +413,16 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    lc.attrs = attr;
     lc.numAttrs = 1;
   }
+  const int pdl_opt = opts ? opts->pdl : 0;
+  if (pdl_opt < -1 || pdl_opt > 1) return GEMM_ERR_INVALID_VALUE;
+  if (pdl_opt == 0 ? kDefaultPdl : pdl_opt > 0) {
+    attr[lc.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[lc.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    ++lc.numAttrs;
+  }
+  lc.attrs = lc.numAttrs ? attr : nullptr;
   cudaError_t e = cudaLaunchKernelEx(&lc, cd.fn[a], tm_a, tm_b, tm_c, p, pm, tm_cpf);
   if (e != cudaSuccess) return cuda_fail(e);
   t_last_launches = 1;

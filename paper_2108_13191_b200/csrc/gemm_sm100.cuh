@@ -240,6 +240,10 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   tc_fence_after();
   uint32_t tmem_base;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot) : "memory");
+  // PDL: everything above (barrier init, TMEM allocation, descriptor prefetch)
+  // overlapped the previous grid's tail; no global memory is touched before this
+  // (bar the diagnostic trace stamps)
+  griddep_wait();
   if (p.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) p.trace[8 * 62 + 1] = globaltimer_ns();
 
   const int cluster = static_cast<int>(blockIdx.x) / CG;
@@ -260,6 +264,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         const int a_row = tm * BM * CG + static_cast<int>(rank) * BM;
         const int b_col = tn * BN + static_cast<int>(rank) * Cfg::BN_CTA;
         const bool backwards = p.k_serpentine && (it & 1);
+        if (tile + nclusters >= p.num_tiles) griddep_launch_dependents();   // last tile: let the next grid ramp
         if (p.c_row_prefetch == 2 && !p.beta0 && !(p.debug_flags & 2) && tile + nclusters < p.num_tiles) {
           // C_in one tile ahead: this CTA's region of the NEXT tile streams into L2
           // under this tile's MMAs, so the epilogue's slot loads hit L2 instead of

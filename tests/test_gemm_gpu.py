@@ -305,3 +305,39 @@ def test_trace_option_records_tiles(g):
     t = tr.cpu().numpy().reshape(64, 8)
     assert t[0, 0] > 0 and t[0, 2] > t[0, 0] and t[0, 7] > 0   # MMA begin/end stamps, cycles
     assert t[62, 0] > 0 and t[62, 2] >= t[62, 0]               # kernel entry/exit of CTA 0
+
+
+@pytest.mark.parametrize("config", ["solo_128x64", "pair_256x256_k128"])
+def test_pdl_dependent_chain_exact(config):
+    """Programmatic dependent launch: a chain of GEMMs that each read the C the
+    previous one wrote, interleaved with torch kernels and inside a CUDA graph, ends
+    bitwise at the closed form (small-integer inputs: every partial sum is exact)."""
+    import torch
+    import paper_2108_13191_b200 as g
+    rng = np.random.default_rng(11)
+    M, N, K = 300, 520, 264
+    A = torch.from_numpy(rng.integers(-2, 3, (M, K)).astype(np.float16)).cuda()
+    B = torch.from_numpy(rng.integers(-2, 3, (K, N)).astype(np.float16)).cuda()
+    C0 = torch.from_numpy(rng.integers(-50, 51, (M, N)).astype(np.float32)).cuda()
+    AB = A.double() @ B.double()
+    C = C0.clone()
+    for _ in range(6):
+        g.gemm_f16(A, B, C, config=config, pdl=1)
+    C.mul_(2)                                    # a torch kernel between PDL launches
+    for _ in range(3):
+        g.gemm_f16(A, B, C, config=config, pdl=1)
+    torch.cuda.synchronize()
+    assert torch.equal(C.double(), 2 * (C0.double() + 6 * AB) + 3 * AB)
+    # captured in a graph
+    C.copy_(C0)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=s):
+        for _ in range(4):
+            g.gemm_f16(A, B, C, config=config, pdl=1)
+    torch.cuda.synchronize()
+    C.copy_(C0)
+    gr.replay(); gr.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(C.double(), C0.double() + 8 * AB)
