@@ -68,7 +68,10 @@ typedef enum {
   GEMM_CFG_PAIR_256x256_S5 = 6, /* as PAIR_256x256, 5 stages, 2 epilogue staging slots per warp */
   GEMM_CFG_PAIR_256x256_S4 = 7, /* as PAIR_256x256, 4 stages, 3 epilogue staging slots per warp */
   GEMM_CFG_PAIR_256x256_K128 = 8, /* as PAIR_256x256 with 128-deep K stages (3 stages)        */
-  GEMM_CFG_COUNT = 9
+  GEMM_CFG_PAIR_256x512 = 9, /* GEMM_ACC_F16 only: cta_group::2, 2 UMMAs 256x256x16 per K step
+                                (256 x 512 pair tile), one TMEM chain over all of K, C_in held
+                                in registers; GEMM_ERR_INVALID_VALUE with GEMM_ACC_F32 */
+  GEMM_CFG_COUNT = 10
 } gemm_config_t;
 
 typedef struct {

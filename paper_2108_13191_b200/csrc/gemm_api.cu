@@ -16,6 +16,7 @@
 
 #include "../../include/gemm_f16.h"
 #include "gemm_sm100.cuh"
+#include "gemm_sm100_wide.cuh"
 
 namespace {
 
@@ -79,8 +80,21 @@ const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
     make_desc<Cfg6F32, Cfg6F16>(),
     make_desc<Cfg7F32, Cfg7F16>(),
     make_desc<Cfg8F32, Cfg8F16>(),
+    ConfigDesc{},   // GEMM_CFG_PAIR_256x512: kWideConfig (defined below)
 };
+using CfgW16 = WCfg<4>;
+const ConfigDesc kWideConfig{2, CfgW16::BN, CfgW16::STAGES, CfgW16::THREADS, CfgW16::BK,
+                             {0, CfgW16::SMEM_BYTES}, {0, CfgW16::CW}, {0, 128},
+                             {nullptr, &gemm_f16_sm100_wide_kernel<CfgW16, false>}};
+// the same tile with the per-element epilogue options (bias, ReLU, accum_f16) compiled in
+const KernelFn kWideExtFn = &gemm_f16_sm100_wide_kernel<CfgW16, true>;
 const ConfigDesc kGatherConfig = make_desc<CfgGF32, CfgGF16>();
+
+const ConfigDesc& config_desc(int c) {
+  if (c == GEMM_CFG_COUNT) return kGatherConfig;
+  if (c == GEMM_CFG_PAIR_256x512) return kWideConfig;
+  return kConfigs[c];
+}
 
 // K elements accumulated in TMEM before the partial sum is promoted to F32
 // registers (R4): 2048 keeps the truncation error near 2.4e-6.
@@ -107,7 +121,8 @@ void init_device(int dev) {
   if (major != 10 || minor != 0) { d.status = GEMM_ERR_UNSUPPORTED_DEVICE; return; }
   for (int c = 1; c <= GEMM_CFG_COUNT; ++c) {
     for (int a = 0; a < 2; ++a) {
-      const ConfigDesc& cd = c == GEMM_CFG_COUNT ? kGatherConfig : kConfigs[c];
+      const ConfigDesc& cd = config_desc(c);
+      if (cd.fn[a] == nullptr) continue;   // not built for this accumulate mode
       e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.fn[a]),
                                cudaFuncAttributeMaxDynamicSharedMemorySize, cd.smem[a]);
       if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
@@ -129,6 +144,11 @@ void init_device(int dev) {
         e = cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(cd.fn[a]), &lc);
         if (e != cudaSuccess || n <= 0) { d.status = GEMM_ERR_CUDA; d.cuda_error = e ? e : cudaErrorInvalidConfiguration; return; }
         d.max_clusters[c][a] = n;
+        if (c == GEMM_CFG_PAIR_256x512) {   // the option-carrying twin: same smem, same cluster
+          e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kWideExtFn),
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, cd.smem[a]);
+          if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
+        }
       } else {
         int per_sm = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cd.fn[a], cd.threads, cd.smem[a]);
@@ -247,12 +267,27 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 //  * when the whole problem is under a third of a wave of pair tiles
 //    (e.g. 1024^3), fixed per-tile latency dominates and the 1-CTA 128x64 tile
 //    (more, shorter tiles) wins (GPU time from CUDA-graph replay);
-//  * a short M (<= 128 rows) wastes too much of a 256-row tile.
+//  * a short M (<= 128 rows) wastes too much of a 256-row tile;
+//  * F16 C: the 256 x 512 pair tile (gemm_sm100_wide.cuh) moves 25 % fewer operand
+//    bytes per FLOP and so sustains a higher clock under the power cap; it wins
+//    wherever its last wave is about as full as the 256 x 256 tile's
+//    (profiles/r01/wide_tile.md: 4096^3 .. 16384^3, 8192^2 x 1024/2048, 4100 x 4096 x 4104,
+//    8192 x 1000 x 1000; it loses at 2048^3 and 32768 x 1024 x 4096 on wave quantization).
 int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
   if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
   const int64_t pair_tiles = cdiv(M, 256) * cdiv(N, 256);
   if (3 * pair_tiles <= sm_count / 2) return GEMM_CFG_SOLO_128x64;
   if (acc_type == GEMM_ACC_F32 && K <= 2048) return GEMM_CFG_PAIR_256x256_S5;
+  if (acc_type == GEMM_ACC_F16) {
+    // the 256 x 512 tile runs 5-10 % faster per wave under the power cap
+    // (profiles/r01/wide_tile.md) but has half as many tiles: take it unless it
+    // fills the last wave of clusters clearly worse than the 256 x 256 tile
+    const int64_t clusters = sm_count / 2;
+    const int64_t wide_tiles = cdiv(M, 256) * cdiv(N, 512);
+    const double eff_pair = double(pair_tiles) / double(cdiv(pair_tiles, clusters) * clusters);
+    const double eff_wide = double(wide_tiles) / double(cdiv(wide_tiles, clusters) * clusters);
+    if (eff_wide + 0.04 >= eff_pair) return GEMM_CFG_PAIR_256x512;
+  }
   return GEMM_CFG_PAIR_256x256_K128;
 }
 
@@ -307,8 +342,9 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (cfg < 0 || cfg >= GEMM_CFG_COUNT) return GEMM_ERR_INVALID_VALUE;
   if (cfg == GEMM_CFG_AUTO) cfg = pick_config(M, N, K, acc_type, di.sm_count);
   if (n_peers > 0) cfg = GEMM_CFG_COUNT;   // fused gather: the peer-store build of PAIR_256x256_K128
-  const ConfigDesc& cd = cfg == GEMM_CFG_COUNT ? kGatherConfig : kConfigs[cfg];
+  const ConfigDesc& cd = config_desc(cfg);
   const int a = acc_type;
+  if (cd.fn[a] == nullptr) return GEMM_ERR_INVALID_VALUE;   // e.g. PAIR_256x512 with F32 C
 
   const int in_type = opts ? opts->in_type : GEMM_IN_F16;
   if (in_type != GEMM_IN_F16 && in_type != GEMM_IN_BF16) return GEMM_ERR_INVALID_VALUE;
@@ -359,6 +395,10 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const int promote = opts ? opts->promote_k : 0;
   if (promote < -1 || (promote > 0 && promote % cd.bk != 0)) return GEMM_ERR_INVALID_VALUE;
   p.kb_per_chunk = promote == -1 ? p.k_blocks : (promote == 0 ? kDefaultPromoteK : promote) / cd.bk;
+  if (cfg == GEMM_CFG_PAIR_256x512) {
+    if (promote > 0) return GEMM_ERR_INVALID_VALUE;   // one TMEM chain over all of K by design
+    p.kb_per_chunk = std::max(p.k_blocks, 1);
+  }
   p.k_chunks = static_cast<int>(cdiv(p.k_blocks, p.kb_per_chunk));
   p.group_m = (opts && opts->group_m > 0) ? opts->group_m : 8;
   if (opts && opts->group_m < 0) return GEMM_ERR_INVALID_VALUE;
@@ -423,7 +463,9 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
     ++lc.numAttrs;
   }
   lc.attrs = lc.numAttrs ? attr : nullptr;
-  cudaError_t e = cudaLaunchKernelEx(&lc, cd.fn[a], tm_a, tm_b, tm_c, p, pm, tm_cpf);
+  KernelFn fn = cd.fn[a];
+  if (cfg == GEMM_CFG_PAIR_256x512 && (p.bias != nullptr || p.relu || p.accum_f16)) fn = kWideExtFn;
+  cudaError_t e = cudaLaunchKernelEx(&lc, fn, tm_a, tm_b, tm_c, p, pm, tm_cpf);
   if (e != cudaSuccess) return cuda_fail(e);
   t_last_launches = 1;
   return GEMM_OK;
@@ -553,7 +595,8 @@ gemm_status_t gemm_f16_config_info(int config, int acc_type, int* tile_m, int* t
                                    int* smem_bytes) {
   if (config <= 0 || config >= GEMM_CFG_COUNT) return GEMM_ERR_INVALID_VALUE;
   if (acc_type != GEMM_ACC_F32 && acc_type != GEMM_ACC_F16) return GEMM_ERR_INVALID_VALUE;
-  const ConfigDesc& cd = kConfigs[config];
+  const ConfigDesc& cd = config_desc(config);
+  if (cd.fn[acc_type] == nullptr) return GEMM_ERR_INVALID_VALUE;
   if (tile_m) *tile_m = 128 * cd.cta_group;
   if (tile_n) *tile_n = cd.tile_n;
   if (cta_group) *cta_group = cd.cta_group;

@@ -24,23 +24,38 @@ def _guarded_dev(host_bits, ld, rows_extra, canary):
 
 @pytest.mark.parametrize("case", range(48))
 def test_fuzz_against_oracle(case):
+    _fuzz_case(case, 10_000 + case, wide=False)
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_fuzz_wide_tile_against_oracle(case):
+    # GEMM_CFG_PAIR_256x512 (F16 C only), larger N so several 512-column tiles occur
+    _fuzz_case(case, 20_000 + case, wide=True)
+
+
+def _fuzz_case(case, seed, wide):
     import torch
     import paper_2108_13191_b200 as g
-    rng = np.random.default_rng(10_000 + case)
+    rng = np.random.default_rng(seed)
     M = int(rng.choice([1, 2, 7, 31, 127, 128, 129, 255, 256, 257]) if rng.random() < 0.3 else rng.integers(1, 700))
     N = int(rng.choice([1, 8, 9, 63, 64, 65, 256, 264]) if rng.random() < 0.3 else rng.integers(1, 700))
     K = int(rng.choice([1, 15, 16, 17, 63, 64, 65, 128, 129]) if rng.random() < 0.3 else rng.integers(1, 1500))
     acc = "f32" if rng.random() < 0.5 else "f16"
     bf16 = rng.random() < 0.25
     kw = {"config": str(rng.choice(CONFIGS))}
+    if wide:
+        acc, kw["config"] = "f16", "pair_256x512"
+        N = int(rng.integers(1, 2600))
     if rng.random() < 0.3:
         kw["max_clusters"] = int(rng.integers(1, 5))
     if rng.random() < 0.3:
         kw["group_m"] = int(rng.integers(1, 9))
     if rng.random() < 0.3:
         kw["acc_bufs"] = 1
-    if rng.random() < 0.3:
+    if rng.random() < 0.3 and not wide:
         kw["promote_k"] = int(rng.choice([-1, 128, 256, 512]))
+    if wide and rng.random() < 0.3:
+        kw["ring_stages"] = int(rng.integers(1, 5))
     if rng.random() < 0.2:
         kw["k_serpentine"] = 1
     beta = 0 if rng.random() < 0.2 else 1

@@ -1,0 +1,229 @@
+"""GPU parity for GEMM_CFG_PAIR_256x512 (the F16-output kernel with a 256 x 512
+CTA-pair tile, csrc/gemm_sm100_wide.cuh) against the CPU oracle.
+
+The kernel keeps one TMEM chain over all of K and holds C_in in registers, so
+the cases below aim at what is new in it: two UMMAs per K step writing the two
+256-column halves of TMEM, the B staging of both halves, the register-resident
+C_in/C_out of each epilogue warp, the single accumulator buffer's phase across
+persistent tiles, and the ragged-N element-wise store.  Bar: F16 rel-Frobenius
+<= 2e-3 (BASELINE.json north_star), closed forms bit-exact.  PAPER.md P:908-909,
+P:967-996."""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity import Guarded, check, device_problem, oracle_full, round_up
+
+pytestmark = pytest.mark.gpu
+
+W = "pair_256x512"
+
+
+@pytest.fixture(scope="module")
+def g():
+    import torch
+    import paper_2108_13191_b200 as g
+    assert torch.cuda.is_available()
+    g.load_library()
+    return g
+
+
+def _run(g, gA, gB, gC, **kw):
+    import torch
+    g.gemm_f16(gA.view, gB.view, gC.view, config=W, **kw)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("shape", [(601, 1100, 333), (256, 512, 64), (257, 513, 65), (1, 1, 1), (1000, 1030, 1000),
+                                   (512, 2048, 1536), (300, 8, 40), (130, 700, 2100)])
+def test_wide_ragged_guarded(g, shape):
+    M, N, K = shape
+    A, B, C, gA, gB, gC = device_problem(M, N, K, "f16", seed=7, pad=(8, 16, 8))
+    _run(g, gA, gB, gC)
+    ex, _ = oracle_full(A, B, C)
+    check(gC.result(), ex, A, B, "f16", K, f"{W} {shape}")
+    assert gC.guard_intact(), "write outside the M x N window"
+    assert gA.guard_intact() and gB.guard_intact()
+
+
+@pytest.mark.parametrize("N", [1001, 1023, 515, 9])
+def test_wide_ragged_n_masked_store(g, N):
+    # N * 2 % 16 != 0: the chunk holding column N-1 is stored element-wise
+    M, K = 390, 200
+    A, B, C, gA, gB, gC = device_problem(M, N, K, "f16", seed=N, pad=(0, 8, 8))
+    _run(g, gA, gB, gC)
+    ex, _ = oracle_full(A, B, C)
+    check(gC.result(), ex, A, B, "f16", K, f"{W} N={N}")
+    assert gC.guard_intact()
+
+
+@pytest.mark.parametrize("max_clusters", [1, 3])
+def test_wide_persistent_phase_wrap(g, max_clusters):
+    # few clusters walk many tiles: the single accumulator buffer's phase, the
+    # ring phase and the C_in staging barrier phase all wrap many times
+    M, N, K = 1300, 2100, 640
+    A, B, C, gA, gB, gC = device_problem(M, N, K, "f16", seed=3)
+    _run(g, gA, gB, gC, max_clusters=max_clusters)
+    ex, _ = oracle_full(A, B, C)
+    check(gC.result(), ex, A, B, "f16", K, f"{W} clusters={max_clusters}")
+
+
+def test_wide_ring_stages_ablation(g):
+    M, N, K = 700, 1500, 900
+    A, B, C = synth.problem(M, N, K, "f16", seed=4)
+    ex, _ = oracle_full(A, B, C)
+    for rs in (1, 2, 3, 4):
+        _, _, _, gA, gB, gC = device_problem(M, N, K, "f16", seed=4)
+        _run(g, gA, gB, gC, ring_stages=rs)
+        check(gC.result(), ex, A, B, "f16", K, f"{W} ring_stages={rs}")
+
+
+def test_wide_closed_forms_bit_exact(g):
+    # identity: A = I (M = K), C_in = 0 -> C = B exactly
+    K, N = 384, 1040
+    B = synth.uniform_f16(3, 1, K, N)
+    gA = Guarded(np.eye(K, dtype=np.float16), K)
+    gB = Guarded(B, N)
+    gC = Guarded(np.zeros((K, N), np.float16), N)
+    _run(g, gA, gB, gC)
+    assert np.array_equal(gC.result().astype(np.float64), B.astype(np.float64))
+    # all ones: C = K exactly (F16 holds every integer <= 2048)
+    for K in (16, 1000, 2048):
+        M, N = 260, 600
+        gA = Guarded(np.ones((M, K), np.float16), K)
+        gB = Guarded(np.ones((K, N), np.float16), N)
+        gC = Guarded(np.zeros((M, N), np.float16), N)
+        _run(g, gA, gB, gC)
+        assert np.all(gC.result() == K), K
+    # small integers with |C| <= 2048: exact in the F32 accumulator and in F16
+    rng = np.random.default_rng(21)
+    M, N, K = 300, 1030, 700
+    Ai = rng.integers(-1, 2, size=(M, K))
+    Bi = rng.integers(-1, 2, size=(K, N))
+    Ci = rng.integers(-100, 101, size=(M, N))
+    gA = Guarded(Ai.astype(np.float16), round_up(K, 8))
+    gB = Guarded(Bi.astype(np.float16), round_up(N, 8))
+    gC = Guarded(Ci.astype(np.float16), round_up(N, 8))
+    _run(g, gA, gB, gC)
+    assert np.array_equal(gC.result().astype(np.int64), Ai @ Bi + Ci)
+    # A = 0 leaves C bitwise unchanged
+    A, Bm, C, gA, gB, gC = device_problem(200, 1100, 96, "f16", seed=4)
+    gA.full.zero_()
+    _run(g, gA, gB, gC)
+    assert np.array_equal(gC.result().view(np.uint8), C.view(np.uint8))
+
+
+def test_wide_permutation_rows(g):
+    # A = P: C = P.B + 0, a pure row gather, so any lane/row mix-up fails bitwise
+    K, N = 512, 1024
+    perm = np.random.default_rng(9).permutation(K)
+    P = np.zeros((K, K), np.float16)
+    P[np.arange(K), perm] = 1
+    B = synth.uniform_f16(0, 1, K, N)
+    gA, gB, gC = Guarded(P, K), Guarded(B, N), Guarded(np.zeros((K, N), np.float16), N)
+    _run(g, gA, gB, gC)
+    assert np.array_equal(gC.result(), B[perm])
+
+
+def test_wide_column_permutation(g):
+    # B = P (column permutation): C = A.P, so each output column is one input column;
+    # catches a swapped B half / TMEM half / epilogue column block bitwise
+    M, K = 384, 1024
+    perm = np.random.default_rng(10).permutation(K)
+    P = np.zeros((K, K), np.float16)
+    P[perm, np.arange(K)] = 1
+    A = synth.uniform_f16(0, 0, M, K)
+    gA, gB, gC = Guarded(A, K), Guarded(P, K), Guarded(np.zeros((M, K), np.float16), K)
+    _run(g, gA, gB, gC)
+    assert np.array_equal(gC.result(), A[:, perm])
+
+
+def test_wide_deterministic_and_schedule_independent(g):
+    import torch
+    M, N, K = 1024, 2048, 1024
+    A, B, C, gA, gB, gC = device_problem(M, N, K, "f16", seed=6)
+    outs = []
+    for mc in (0, 0, 1, 5):
+        gC.full.copy_(torch.from_numpy(gC.full_host.copy()))
+        _run(g, gA, gB, gC, max_clusters=mc)
+        outs.append(gC.result().copy())
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint16), outs[0].view(np.uint16))
+
+
+CASES = list(itertools.product(["f16", "bf16"], [1, 0], [False, True], [False, True]))
+
+
+@pytest.mark.parametrize("in_t,beta,use_bias,relu", CASES)
+def test_wide_fused_epilogue(g, in_t, beta, use_bias, relu):
+    import torch
+    M, N, K = 520, 1100, 777
+    if in_t == "bf16":
+        A, B, C = synth.problem_bf16(M, N, K, "f16", seed=50)
+        dA = torch.from_numpy(A.view(np.int16)).view(torch.bfloat16)
+        dB = torch.from_numpy(B.view(np.int16)).view(torch.bfloat16)
+        pad = lambda t, ld: torch.nn.functional.pad(t.view(torch.int16), (0, ld - t.shape[1])).view(t.dtype)
+    else:
+        A, B, C = synth.problem(M, N, K, "f16", seed=50)
+        dA, dB = torch.from_numpy(A), torch.from_numpy(B)
+        pad = lambda t, ld: torch.nn.functional.pad(t, (0, ld - t.shape[1]))
+    dA = pad(dA, round_up(K, 8) + 8).cuda()[:, :K]
+    dB = pad(dB, round_up(N, 8) + 8).cuda()[:, :N]
+    dC = torch.nn.functional.pad(torch.from_numpy(C), (0, round_up(N, 8) + 8 - N)).cuda()[:, :N]
+    bias = synth.uniform_f32(51, 3, 1, N)[0] * np.float32(4.0) if use_bias else None
+    dbias = torch.from_numpy(bias).cuda() if use_bias else None
+    g.gemm_f16(dA, dB, dC, config=W, beta=beta, bias=dbias, relu=relu)
+    torch.cuda.synchronize()
+    ex, _ = oracle.gemm(A, B, C, in_type=1 if in_t == "bf16" else 0, beta=beta, bias=bias, relu=relu)
+    Av = A if in_t == "f16" else torch.from_numpy(A.view(np.int16)).view(torch.bfloat16).float().numpy()
+    Bv = B if in_t == "f16" else torch.from_numpy(B.view(np.int16)).view(torch.bfloat16).float().numpy()
+    check(dC.cpu().numpy(), ex, Av, Bv, "f16", K, f"{W} {in_t} beta={beta} bias={use_bias} relu={relu}")
+    if relu:
+        assert (dC.cpu().numpy() >= 0).all()
+
+
+def test_wide_rejects_f32_and_promotion(g):
+    import torch
+    A = torch.zeros((256, 64), dtype=torch.float16, device="cuda")
+    B = torch.zeros((64, 512), dtype=torch.float16, device="cuda")
+    C32 = torch.zeros((256, 512), dtype=torch.float32, device="cuda")
+    C16 = torch.zeros((256, 512), dtype=torch.float16, device="cuda")
+    with pytest.raises(g.GemmError):
+        g.gemm_f16(A, B, C32, config=W)
+    with pytest.raises(g.GemmError):
+        g.gemm_f16(A, B, C16, config=W, promote_k=1024)
+    info = g.config_info(W, g.ACC_F16)
+    assert info["tile_m"] == 256 and info["tile_n"] == 512 and info["cta_group"] == 2
+
+
+@pytest.mark.parametrize("K", [4096, 16384])
+def test_wide_long_k_single_chain_error(g, K):
+    # one TMEM chain over all of K: the truncation error (R4, ~1.2e-6 per
+    # 1024 of K) stays two orders under the F16 bar; the F16 rounding dominates
+    import torch
+    M, N = 256, 1024
+    A, B, C = synth.problem(M, N, K, "f16", seed=8)
+    dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+    g.gemm_f16(dA, dB, dC, config=W)
+    torch.cuda.synchronize()
+    ex, _ = oracle.gemm(A, B, C)
+    s = check(dC.cpu().numpy(), ex, A, B, "f16", K, f"{W} K={K}")
+    assert s["rel_fro"] < 4e-4, s
+
+
+def test_wide_8192_cube_sampled(g):
+    # BASELINE's metric shape, F16 mode, in this config
+    import torch
+    M = N = K = 8192
+    A, B, C = synth.problem(M, N, K, "f16", seed=0)
+    dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+    g.gemm_f16(dA, dB, dC, config=W)
+    torch.cuda.synchronize()
+    rows = synth.sample_rows(M, tile_m=128, n_random=24, seed=0)
+    rows = rows[np.linspace(0, len(rows) - 1, 64).astype(int)]
+    got = dC[torch.from_numpy(rows).cuda()].cpu().numpy()
+    ex, _ = oracle.gemm(A, B, C, rows=rows)
+    check(got, ex, A[rows], B, "f16", K, "8192^3 wide sampled")
