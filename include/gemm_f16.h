@@ -180,6 +180,10 @@ gemm_status_t gemm_f16_gather(int64_t M, int64_t N, int64_t K,
  * later work on `stream` is ordered after it.  Host buffers should be
  * page-locked for the copies to be asynchronous.  The caller synchronises
  * `stream` before reading hC.
+ * Resident operands: hA == NULL (resp. hB == NULL) means A (resp. B) is already
+ * in dA (dB), written by work ordered before this call on `stream` -- e.g. two
+ * GEMMs on the same operands copy A and B once; lda (ldb) is then ignored.
+ * hC may not be NULL.
  */
 gemm_status_t gemm_f16_host(int64_t M, int64_t N, int64_t K,
                             const void* hA, int64_t lda,

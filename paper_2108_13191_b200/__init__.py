@@ -244,16 +244,23 @@ def gemm_f16_host(hA, hB, hC, dA, dB, dC, stream=None):
     """End-to-end path: host (pinned) A, B, C -> device scratch -> GEMM -> C back to host.
 
     hA/hB/hC are CPU torch tensors (float16 / float16 / float32|float16); dA/dB/dC
-    are CUDA scratch tensors of the same shapes and dtypes.  Enqueued on `stream`;
-    the caller synchronises before reading hC.
+    are CUDA scratch tensors of the same shapes and dtypes.  hA or hB may be None:
+    that operand is already resident in dA / dB (e.g. a second GEMM on the same
+    operands).  Enqueued on `stream`; the caller synchronises before reading hC.
     """
     import torch
     lib = load_library()
     acc = _acc_of(hC)
-    M, K = hA.shape
-    _, N = hB.shape
+    M, K = dA.shape
+    _, N = dB.shape
+    pA = 0 if hA is None else hA.data_ptr()
+    pB = 0 if hB is None else hB.data_ptr()
+    lA = 0 if hA is None else _ld(hA, "hA")
+    lB = 0 if hB is None else _ld(hB, "hB")
+    if hA is not None and tuple(hA.shape) != (M, K) or hB is not None and tuple(hB.shape) != (K, N):
+        raise ValueError("host and device operand shapes differ")
     with torch.cuda.device(dC.device):
-        st = lib.gemm_f16_host(M, N, K, hA.data_ptr(), _ld(hA, "hA"), hB.data_ptr(), _ld(hB, "hB"),
+        st = lib.gemm_f16_host(M, N, K, pA, lA, pB, lB,
                                hC.data_ptr(), _ld(hC, "hC"), acc,
                                dA.data_ptr(), _ld(dA, "dA"), dB.data_ptr(), _ld(dB, "dB"),
                                dC.data_ptr(), _ld(dC, "dC"), _stream_handle(stream, dC.device.index))

@@ -520,8 +520,9 @@ gemm_status_t gemm_f16_host(int64_t M, int64_t N, int64_t K, const void* hA, int
   bool no_work = false;
   gemm_status_t st = validate(M, N, K, dA, ldda, dB, lddb, dC, lddc, acc_type, &no_work);
   if (st != GEMM_OK || no_work) return st;
-  if (!hA || !hB || !hC) return GEMM_ERR_INVALID_VALUE;
-  if (lda < std::max<int64_t>(1, K) || ldb < std::max<int64_t>(1, N) || ldc < std::max<int64_t>(1, N))
+  if (!hC) return GEMM_ERR_INVALID_VALUE;   // hA / hB == NULL: operand already resident in dA / dB
+  if ((hA && lda < std::max<int64_t>(1, K)) || (hB && ldb < std::max<int64_t>(1, N)) ||
+      ldc < std::max<int64_t>(1, N))
     return GEMM_ERR_INVALID_VALUE;
   int dev = 0;
   st = device_ready(&dev);
@@ -550,15 +551,17 @@ gemm_status_t gemm_f16_host(int64_t M, int64_t N, int64_t K, const void* hA, int
   e = cudaEventRecord(ev_start, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(hs.h2d, ev_start, 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(hs.d2h, ev_start, 0);
-  if (e == cudaSuccess) e = cudaMemcpy2DAsync(dB, lddb * 2, hB, ldb * 2, N * 2, K, cudaMemcpyHostToDevice, hs.h2d);
+  if (e == cudaSuccess && hB) e = cudaMemcpy2DAsync(dB, lddb * 2, hB, ldb * 2, N * 2, K, cudaMemcpyHostToDevice, hs.h2d);
   int launches = 0;
   for (int64_t j = 0; j < nblk && e == cudaSuccess; ++j) {
     const int64_t r0 = j * rb, mj = std::min(rb, M - r0);
-    const char* hAj = static_cast<const char*>(hA) + r0 * lda * 2;
     char* dAj = static_cast<char*>(dA) + r0 * ldda * 2;
     char* hCj = static_cast<char*>(hC) + r0 * ldc * csz;
     char* dCj = static_cast<char*>(dC) + r0 * lddc * csz;
-    e = cudaMemcpy2DAsync(dAj, ldda * 2, hAj, lda * 2, K * 2, mj, cudaMemcpyHostToDevice, hs.h2d);
+    if (hA) {
+      const char* hAj = static_cast<const char*>(hA) + r0 * lda * 2;
+      e = cudaMemcpy2DAsync(dAj, ldda * 2, hAj, lda * 2, K * 2, mj, cudaMemcpyHostToDevice, hs.h2d);
+    }
     if (e == cudaSuccess) e = cudaMemcpy2DAsync(dCj, lddc * csz, hCj, ldc * csz, N * csz, mj, cudaMemcpyHostToDevice, hs.h2d);
     if (e == cudaSuccess) e = cudaEventRecord(ev_in[j], hs.h2d);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_in[j], 0);

@@ -269,6 +269,37 @@ def test_host_path_row_block_pipeline(g, M):
         check(hC.numpy(), ex, A, B, acc, K, f"host pipeline M={M}")
 
 
+@pytest.mark.parametrize("M", [700, 3000])
+def test_host_path_resident_operands(g, M):
+    """gemm_f16_host with hA/hB = None reuses A/B already in dA/dB (the bench's e2e
+    step: one F32 and one F16 GEMM on the same operands copy A and B once); dA/dB
+    are poisoned before the first call so a missed copy cannot pass."""
+    import torch
+    N, K = 520, 264
+    A, B, C32 = synth.problem(M, N, K, "f32", seed=M + 1)
+    _, _, C16 = synth.problem(M, N, K, "f16", seed=M + 1)
+    hA = torch.from_numpy(A).pin_memory()
+    hB = torch.from_numpy(B).pin_memory()
+    hC32 = torch.from_numpy(C32.copy()).pin_memory()
+    hC16 = torch.from_numpy(C16.copy()).pin_memory()
+    dA = torch.full((M, K), float("nan"), dtype=torch.float16, device="cuda")
+    dB = torch.full((K, N), float("nan"), dtype=torch.float16, device="cuda")
+    dC32 = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    dC16 = torch.empty((M, N), dtype=torch.float16, device="cuda")
+    s = torch.cuda.Stream()
+    g.gemm_f16_host(hA, hB, hC32, dA, dB, dC32, stream=s)
+    g.gemm_f16_host(None, None, hC16, dA, dB, dC16, stream=s)
+    s.synchronize()
+    check(hC32.numpy(), oracle_full(A, B, C32)[0], A, B, "f32", K, "host, A/B copied")
+    check(hC16.numpy(), oracle_full(A, B, C16)[0], A, B, "f16", K, "host, A/B resident")
+    # only B resident: a new A is copied, the old B reused
+    A2 = synth.uniform_f16(M + 7, 0, M, K)
+    hC16b = torch.from_numpy(C16.copy()).pin_memory()
+    g.gemm_f16_host(torch.from_numpy(A2).pin_memory(), None, hC16b, dA, dB, dC16, stream=s)
+    s.synchronize()
+    check(hC16b.numpy(), oracle_full(A2, B, C16)[0], A2, B, "f16", K, "host, B resident")
+
+
 def test_cuda_graph_capture_replay(g):
     """The C ABI is capturable: gemm_f16 calls recorded into a CUDA graph replay
     to the same results as eager calls (tensor maps travel as kernel params)."""
