@@ -71,7 +71,14 @@ typedef enum {
   GEMM_CFG_PAIR_256x512 = 9, /* GEMM_ACC_F16 only: cta_group::2, 2 UMMAs 256x256x16 per K step
                                 (256 x 512 pair tile), one TMEM chain over all of K, C_in held
                                 in registers; GEMM_ERR_INVALID_VALUE with GEMM_ACC_F32 */
-  GEMM_CFG_COUNT = 10
+  GEMM_CFG_SPLITK_128x256_S2 = 10, /* split-K over a 2-CTA cluster: cta_group::1 UMMA 128x256x16, each
+                                      CTA one half of K, partials reduced through distributed shared
+                                      memory (fixed order, no workspace); one tile per cluster.  Each
+                                      CTA keeps one TMEM chain over its K / S (promote_k must be 0 or
+                                      -1): with F32 C, K / S > 8192 exceeds the 1e-5 error bar */
+  GEMM_CFG_SPLITK_128x256_S4 = 11, /* as SPLITK_128x256_S2 with 4 CTAs (quarters of K) per cluster */
+  GEMM_CFG_SPLITK_128x128_S4 = 12, /* as SPLITK_128x256_S4 with UMMA 128x128x16 tiles */
+  GEMM_CFG_COUNT = 13
 } gemm_config_t;
 
 typedef struct {

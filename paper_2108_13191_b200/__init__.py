@@ -33,6 +33,9 @@ CONFIGS = {
     "pair_256x256_s4": 7,
     "pair_256x256_k128": 8,
     "pair_256x512": 9,   # F16 C only
+    "splitk_128x256_s2": 10,
+    "splitk_128x256_s4": 11,
+    "splitk_128x128_s4": 12,
 }
 _STATUS = {0: "GEMM_OK", 1: "GEMM_ERR_INVALID_VALUE", 2: "GEMM_ERR_MISALIGNED",
            3: "GEMM_ERR_UNSUPPORTED_DEVICE", 4: "GEMM_ERR_CUDA"}

@@ -17,6 +17,7 @@
 #include "../../include/gemm_f16.h"
 #include "gemm_sm100.cuh"
 #include "gemm_sm100_wide.cuh"
+#include "gemm_sm100_splitk.cuh"
 
 namespace {
 
@@ -61,6 +62,9 @@ struct ConfigDesc {
   int c_box_cols[2];  // epilogue staging box width (elements)
   int c_row_bytes[2]; // 128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B
   KernelFn fn[2];
+  int cluster = 0;    // CTAs per cluster (0: = cta_group)
+  int k_splits = 0;   // split-K configs: CTAs per cluster sharing one tile's K (non-persistent grid)
+  int csize(int a) const { return cluster ? cluster : cta_group; }
 };
 
 template <class C32, class C16>
@@ -68,6 +72,15 @@ constexpr ConfigDesc make_desc() {
   return ConfigDesc{C32::CG, C32::BN, C32::STAGES, C32::THREADS, C32::BK,
                     {C32::SMEM_BYTES, C16::SMEM_BYTES}, {C32::CW, C16::CW}, {C32::RB, C16::RB},
                     {&gemm_f16_sm100_kernel<C32>, &gemm_f16_sm100_kernel<C16>}};
+}
+
+template <int BN, int S>
+constexpr ConfigDesc make_splitk_desc() {
+  using C32 = SKCfg<BN, S, false>;
+  using C16 = SKCfg<BN, S, true>;
+  return ConfigDesc{1, BN, C32::STAGES, C32::THREADS, C32::BK,
+                    {C32::SMEM_BYTES, C16::SMEM_BYTES}, {32, 64}, {128, 128},
+                    {&gemm_f16_sm100_splitk_kernel<C32>, &gemm_f16_sm100_splitk_kernel<C16>}, S, S};
 }
 
 const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
@@ -81,6 +94,9 @@ const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
     make_desc<Cfg7F32, Cfg7F16>(),
     make_desc<Cfg8F32, Cfg8F16>(),
     ConfigDesc{},   // GEMM_CFG_PAIR_256x512: kWideConfig (defined below)
+    make_splitk_desc<256, 2>(),
+    make_splitk_desc<256, 4>(),
+    make_splitk_desc<128, 4>(),
 };
 using CfgW16 = WCfg<4>;
 const ConfigDesc kWideConfig{2, CfgW16::BN, CfgW16::STAGES, CfgW16::THREADS, CfgW16::BK,
@@ -126,16 +142,17 @@ void init_device(int dev) {
       e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.fn[a]),
                                cudaFuncAttributeMaxDynamicSharedMemorySize, cd.smem[a]);
       if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
-      if (cd.cta_group == 2) {
+      const int cs = cd.csize(a);
+      if (cs > 1) {
         e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.fn[a]),
                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
         cudaLaunchConfig_t lc = {};
         cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.x = cs;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
-        lc.gridDim = dim3(2 * (d.sm_count / 2), 1, 1);
+        lc.gridDim = dim3(cs * (d.sm_count / cs), 1, 1);
         lc.blockDim = dim3(cd.threads, 1, 1);
         lc.dynamicSmemBytes = cd.smem[a];
         lc.attrs = attr;
@@ -268,15 +285,28 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 //    (e.g. 1024^3), fixed per-tile latency dominates and the 1-CTA 128x64 tile
 //    (more, shorter tiles) wins (GPU time from CUDA-graph replay);
 //  * a short M (<= 128 rows) wastes too much of a 256-row tile;
+//  * a small output with a long K (e.g. 512^2 x 2048, 1024^2 x 4096) is split over
+//    K across a cluster (gemm_sm100_splitk.cuh), S CTAs per tile;
 //  * F16 C: the 256 x 512 pair tile (gemm_sm100_wide.cuh) moves 25 % fewer operand
 //    bytes per FLOP and so sustains a higher clock under the power cap; it wins
 //    wherever its last wave is about as full as the 256 x 256 tile's
 //    (profiles/r01/wide_tile.md: 4096^3 .. 16384^3, 8192^2 x 1024/2048, 4100 x 4096 x 4104,
 //    8192 x 1000 x 1000; it loses at 2048^3 and 32768 x 1024 x 4096 on wave quantization).
 int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
-  if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
   const int64_t pair_tiles = cdiv(M, 256) * cdiv(N, 256);
-  if (3 * pair_tiles <= sm_count / 2) return GEMM_CFG_SOLO_128x64;
+  if (M <= 128 || 3 * pair_tiles <= sm_count / 2) {
+    // small output: split K over a cluster when K is long enough to pay for the
+    // DSMEM reduction (profiles/r01/splitk.md; it loses at K <= 2048 with 1024^2)
+    // Each CTA keeps one truncating TMEM chain over its K / S (no promotion, R4):
+    // for F32 C that chain stays <= 4096 long (rel. error <~ 5e-6, bar 1e-5).
+    const int64_t kmax_chain = acc_type == GEMM_ACC_F32 ? 4096 : INT64_MAX;
+    const int64_t t128 = cdiv(M, 128) * cdiv(N, 128), t256 = cdiv(M, 128) * cdiv(N, 256);
+    if (K >= 2048 && 4 * t128 <= sm_count && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x128_S4;
+    if (K >= 8192 && 4 * t256 <= sm_count && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S4;
+    if (K >= 4096 && 2 * t256 <= sm_count && K <= 2 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S2;
+    if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
+    return GEMM_CFG_SOLO_128x64;
+  }
   if (acc_type == GEMM_ACC_F32 && K <= 2048) return GEMM_CFG_PAIR_256x256_S5;
   if (acc_type == GEMM_ACC_F16) {
     // the 256 x 512 tile runs 5-10 % faster per wave under the power cap
@@ -363,9 +393,11 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (!ok) return cuda_fail(cudaErrorInvalidValue);
   // C_in L2-prefetch map: one box = an epilogue warp's whole region (32 rows x tile_n/2
   // columns), unswizzled -- it only drives cp.async.bulk.prefetch, never smem
+  // (split-K configs: the C_in slice one CTA reduces, tile_n / k_splits columns x 128 rows, loaded by TMA)
   CUtensorMap tm_cpf;
   if (!encode_2d(&tm_cpf, acc_type == GEMM_ACC_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                 acc_type == GEMM_ACC_F32 ? 4 : 2, C, M, N, ldc, static_cast<uint32_t>(cd.tile_n / 2), 32,
+                 acc_type == GEMM_ACC_F32 ? 4 : 2, C, M, N, ldc,
+                 static_cast<uint32_t>(cd.k_splits ? cd.tile_n / cd.k_splits : cd.tile_n / 2), cd.k_splits ? 128 : 32,
                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cuda_fail(cudaErrorInvalidValue);
   PeerMaps pm;
@@ -386,19 +418,21 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   p.N = static_cast<int>(N);
   p.K = static_cast<int>(K);
   const int tile_m = 128 * cd.cta_group;
+  const int cl_size = cd.csize(a);
   p.tiles_m = static_cast<int>(cdiv(M, tile_m));
   p.tiles_n = static_cast<int>(cdiv(N, cd.tile_n));
   const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n;
-  if (tiles > 0x7fffffffLL) return GEMM_ERR_INVALID_VALUE;
+  if (tiles * std::max(1, cd.csize(a)) > 0x7fffffffLL) return GEMM_ERR_INVALID_VALUE;
   p.num_tiles = static_cast<int>(tiles);
   p.k_blocks = static_cast<int>(cdiv(K, cd.bk));
   const int promote = opts ? opts->promote_k : 0;
   if (promote < -1 || (promote > 0 && promote % cd.bk != 0)) return GEMM_ERR_INVALID_VALUE;
   p.kb_per_chunk = promote == -1 ? p.k_blocks : (promote == 0 ? kDefaultPromoteK : promote) / cd.bk;
-  if (cfg == GEMM_CFG_PAIR_256x512) {
-    if (promote > 0) return GEMM_ERR_INVALID_VALUE;   // one TMEM chain over all of K by design
+  if (cfg == GEMM_CFG_PAIR_256x512 || cd.k_splits) {
+    if (promote > 0) return GEMM_ERR_INVALID_VALUE;   // one TMEM chain over all of K (its share) by design
     p.kb_per_chunk = std::max(p.k_blocks, 1);
   }
+  p.k_splits = cd.k_splits;
   p.k_chunks = static_cast<int>(cdiv(p.k_blocks, p.kb_per_chunk));
   p.group_m = (opts && opts->group_m > 0) ? opts->group_m : 8;
   if (opts && opts->group_m < 0) return GEMM_ERR_INVALID_VALUE;
@@ -441,16 +475,17 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (opts && opts->max_clusters > 0) clusters = opts->max_clusters;
   if (opts && opts->max_clusters < 0) return GEMM_ERR_INVALID_VALUE;
   clusters = static_cast<int>(std::min<int64_t>(clusters, tiles));
+  if (cd.k_splits) clusters = static_cast<int>(tiles);   // one tile per cluster (non-persistent)
 
   cudaLaunchConfig_t lc = {};
   cudaLaunchAttribute attr[2];
-  lc.gridDim = dim3(static_cast<unsigned>(clusters * cd.cta_group), 1, 1);
+  lc.gridDim = dim3(static_cast<unsigned>(clusters * cl_size), 1, 1);
   lc.blockDim = dim3(static_cast<unsigned>(cd.threads), 1, 1);
   lc.dynamicSmemBytes = cd.smem[a];
   lc.stream = stream;
-  if (cd.cta_group == 2) {
+  if (cl_size > 1) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = cl_size;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     lc.numAttrs = 1;

@@ -52,6 +52,8 @@ struct GemmParams {
   int k_blocks;                     // ceil(K / BK): smem ring stages per tile
   int kb_per_chunk;                 // k-blocks accumulated in TMEM before promotion to registers
   int k_chunks;                     // ceil(k_blocks / kb_per_chunk)
+  int k_splits;                     // split-K kernels (gemm_sm100_splitk.cuh): CTAs per cluster,
+                                    // each accumulating a contiguous share of the k-blocks
   int group_m;                      // raster group height in tiles
   int c_ragged;                     // N * sizeof(C) % 16 != 0: TMA stores would write a
                                     // whole 16-byte granule past column N-1, so the chunk

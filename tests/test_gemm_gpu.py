@@ -223,7 +223,7 @@ def test_promotion_bounds_long_k_error(g):
     rel = {}
     for pk in (0, -1):
         dC = torch.from_numpy(C.copy()).cuda()
-        g.gemm_f16(dA, dB, dC, promote_k=pk)
+        g.gemm_f16(dA, dB, dC, promote_k=pk, config="pair_256x256")   # (auto would split K here)
         torch.cuda.synchronize()
         rel[pk] = stats(dC.cpu().numpy(), ex)["rel_fro"]
     print(f"K=16384 rel_fro: promoted {rel[0]:.3e}, single chain {rel[-1]:.3e}")

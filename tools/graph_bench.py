@@ -4,7 +4,8 @@ import os, sys, json, statistics
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import torch, synth
 import paper_2108_13191_b200 as g
-shapes = [(256, 256, 256), (512, 512, 512), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 1024, 1024), (2048, 2048, 512)]
+shapes = [tuple(int(x) for x in t.split("x")) for t in os.environ.get("SHAPES", "256x256x256,512x512x512,1024x1024x1024,2048x2048x2048,4096x1024x1024,2048x2048x512").split(",")]
+CFGS = [int(c) for c in os.environ.get("CFGS", "1,2,4,5,6").split(",")]
 R = 20
 for (M, N, K) in shapes:
     for mode in ("f32", "f16"):
@@ -12,7 +13,7 @@ for (M, N, K) in shapes:
         B = torch.from_numpy(synth.uniform_f16(0, 1, K, N)).cuda()
         C = torch.from_numpy((synth.uniform_f32 if mode == "f32" else synth.uniform_f16)(0, 2, M, N)).cuda()
         row = {"shape": [M, N, K], "mode": mode, "auto": g.pick_config(M, N, K, 0 if mode == "f32" else 1)}
-        for cfg in (1, 2, 4, 5, 6):
+        for cfg in CFGS:
             s = torch.cuda.Stream()
             with torch.cuda.stream(s):
                 for _ in range(3): g.gemm_f16(A, B, C, config=cfg)
