@@ -120,6 +120,9 @@ typedef struct {
   int pdl;          /* 0: default; 1: programmatic dependent launch (the kernel's prologue */
                     /* overlaps the previous grid's tail in the stream; it waits for that  */
                     /* grid before touching global memory); -1: off                        */
+  int raster;       /* 0: default; 1: serpentine raster -- odd groups of group_m tile-rows */
+                    /* walk their column strips right to left, so the B columns the last  */
+                    /* wave of a group used are the first the next group needs; -1: plain */
 } gemm_options_t;
 
 /*

@@ -29,6 +29,7 @@ constexpr int kDefaultKSerpentine = 0;
 constexpr unsigned kDefaultWaitHintNs = 0;
 constexpr int kDefaultCRowPrefetch = 0;
 constexpr int kDefaultPdl = 1;   // profiles/r01/findings.md section 9
+constexpr int kDefaultSnake = 0;
 
 thread_local int t_last_cuda_error = 0;
 thread_local int t_last_launches = 0;
@@ -490,6 +491,9 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
     attr[0].val.clusterDim.z = 1;
     lc.numAttrs = 1;
   }
+  const int raster = opts ? opts->raster : 0;
+  if (raster < -1 || raster > 1) return GEMM_ERR_INVALID_VALUE;
+  p.snake = raster == 0 ? kDefaultSnake : (raster > 0 ? 1 : 0);
   const int pdl_opt = opts ? opts->pdl : 0;
   if (pdl_opt < -1 || pdl_opt > 1) return GEMM_ERR_INVALID_VALUE;
   if (pdl_opt == 0 ? kDefaultPdl : pdl_opt > 0) {

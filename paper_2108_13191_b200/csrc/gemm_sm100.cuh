@@ -55,6 +55,7 @@ struct GemmParams {
   int k_splits;                     // split-K kernels (gemm_sm100_splitk.cuh): CTAs per cluster,
                                     // each accumulating a contiguous share of the k-blocks
   int group_m;                      // raster group height in tiles
+  int snake;                        // 1: odd raster groups walk their columns right to left
   int c_ragged;                     // N * sizeof(C) % 16 != 0: TMA stores would write a
                                     // whole 16-byte granule past column N-1, so the chunk
                                     // holding column N-1 is stored element-wise instead
@@ -170,6 +171,7 @@ __device__ __forceinline__ void tile_coords(int tile, const GemmParams& p, int& 
   const int local = tile - g * per_group;
   tm = first + local % gs;
   tn = local / gs;
+  if (p.snake && (g & 1)) tn = p.tiles_n - 1 - tn;
 }
 
 // Byte offset of 16-byte unit j of row r in a TMA-swizzled staging box whose

@@ -232,7 +232,8 @@ def test_promotion_bounds_long_k_error(g):
 
 @pytest.mark.parametrize("kw", [
     {"ring_stages": 1}, {"ring_stages": 2}, {"acc_bufs": 1}, {"acc_bufs": 1, "ring_stages": 1},
-    {"group_m": 1}, {"group_m": 3}, {"l2_hints": -1}, {"epi_pace": -1}, {"max_clusters": 1000},
+    {"group_m": 1}, {"group_m": 3}, {"raster": 1}, {"raster": 1, "group_m": 2}, {"l2_hints": -1}, {"epi_pace": -1},
+    {"max_clusters": 1000},
     {"config": "pair_256x256_s5"}, {"config": "pair_256x256_s4"}, {"config": "solo_128x256", "ring_stages": 1, "acc_bufs": 1},
     {"k_serpentine": 1, "max_clusters": 2}, {"wait_hint_ns": 20000}, {"epi_pace": 1},
 ])

@@ -146,9 +146,9 @@ def test_wide_deterministic_and_schedule_independent(g):
     M, N, K = 1024, 2048, 1024
     A, B, C, gA, gB, gC = device_problem(M, N, K, "f16", seed=6)
     outs = []
-    for mc in (0, 0, 1, 5):
+    for mc, raster in ((0, 0), (0, 0), (1, 0), (5, 0), (0, 1), (3, 1)):
         gC.full.copy_(torch.from_numpy(gC.full_host.copy()))
-        _run(g, gA, gB, gC, max_clusters=mc)
+        _run(g, gA, gB, gC, max_clusters=mc, raster=raster)
         outs.append(gC.result().copy())
     for o in outs[1:]:
         assert np.array_equal(o.view(np.uint16), outs[0].view(np.uint16))
