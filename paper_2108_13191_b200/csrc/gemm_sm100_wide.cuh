@@ -179,6 +179,8 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
           umma_f16<2>(tmem_base + static_cast<uint32_t>(h * Cfg::UMMA_N), desc_sw128(a_s + 32 * k, 16, 1024),
                       desc_sw128(b_s + 2048 * k, Cfg::B_ATOM_BYTES, 1024), idesc, (first && k == 0) ? 0u : 1u);
       };
+      // split k-blocks per tile end: ring_stages - 1 leaves one stage for the next tile's
+      // first load (all 4 stages measured equal within noise, +1 % / -0.2 %)
       const int split_max = p.ring_stages > 1 ? p.ring_stages - 1 : 1;
       int stage = 0;
       uint32_t phase = 0;
