@@ -65,7 +65,7 @@ struct ConfigDesc {
   KernelFn fn[2];
   int cluster = 0;    // CTAs per cluster (0: = cta_group)
   int k_splits = 0;   // split-K configs: CTAs per cluster sharing one tile's K (non-persistent grid)
-  int csize(int a) const { return cluster ? cluster : cta_group; }
+  int cluster_size() const { return cluster ? cluster : cta_group; }
 };
 
 template <class C32, class C16>
@@ -143,7 +143,7 @@ void init_device(int dev) {
       e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.fn[a]),
                                cudaFuncAttributeMaxDynamicSharedMemorySize, cd.smem[a]);
       if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
-      const int cs = cd.csize(a);
+      const int cs = cd.cluster_size();
       if (cs > 1) {
         e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.fn[a]),
                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
@@ -419,11 +419,11 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   p.N = static_cast<int>(N);
   p.K = static_cast<int>(K);
   const int tile_m = 128 * cd.cta_group;
-  const int cl_size = cd.csize(a);
+  const int cl_size = cd.cluster_size();
   p.tiles_m = static_cast<int>(cdiv(M, tile_m));
   p.tiles_n = static_cast<int>(cdiv(N, cd.tile_n));
   const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n;
-  if (tiles * std::max(1, cd.csize(a)) > 0x7fffffffLL) return GEMM_ERR_INVALID_VALUE;
+  if (tiles * std::max(1, cd.cluster_size()) > 0x7fffffffLL) return GEMM_ERR_INVALID_VALUE;
   p.num_tiles = static_cast<int>(tiles);
   p.k_blocks = static_cast<int>(cdiv(K, cd.bk));
   const int promote = opts ? opts->promote_k : 0;
