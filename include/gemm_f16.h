@@ -78,7 +78,10 @@ typedef enum {
                                       -1): with F32 C, K / S > 8192 exceeds the 1e-5 error bar */
   GEMM_CFG_SPLITK_128x256_S4 = 11, /* as SPLITK_128x256_S2 with 4 CTAs (quarters of K) per cluster */
   GEMM_CFG_SPLITK_128x128_S4 = 12, /* as SPLITK_128x256_S4 with UMMA 128x128x16 tiles */
-  GEMM_CFG_COUNT = 13
+  GEMM_CFG_SOLO_128x64_MC4 = 13,  /* as SOLO_128x64 in 4-CTA clusters along N: each CTA loads a quarter
+                                     of the shared A box and TMA-multicasts it to the other three */
+  GEMM_CFG_SOLO_128x128_MC4 = 14, /* as SOLO_128x128, with the same A multicast */
+  GEMM_CFG_COUNT = 15
 } gemm_config_t;
 
 typedef struct {

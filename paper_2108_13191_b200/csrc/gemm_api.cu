@@ -50,6 +50,11 @@ using Cfg7F32 = KCfg<2, 256, 4, false, 3>;
 using Cfg7F16 = KCfg<2, 256, 4, true, 3>;
 using Cfg8F32 = KCfg<2, 256, 3, false, 1, 128>;
 using Cfg8F16 = KCfg<2, 256, 3, true, 1, 128>;
+// A multicast across a 4-CTA cluster of 1-CTA tiles along N (small problems)
+using Cfg13F32 = KCfg<1, 64, 8, false, 1, 64, false, 4>;
+using Cfg13F16 = KCfg<1, 64, 8, true, 1, 64, false, 4>;
+using Cfg14F32 = KCfg<1, 128, 6, false, 1, 64, false, 4>;
+using Cfg14F16 = KCfg<1, 128, 6, true, 1, 64, false, 4>;
 // gemm_f16_gather: the 128-deep pair tile with peer stores compiled in
 using CfgGF32 = KCfg<2, 256, 3, false, 1, 128, true>;
 using CfgGF16 = KCfg<2, 256, 3, true, 1, 128, true>;
@@ -65,6 +70,7 @@ struct ConfigDesc {
   KernelFn fn[2];
   int cluster = 0;    // CTAs per cluster (0: = cta_group)
   int k_splits = 0;   // split-K configs: CTAs per cluster sharing one tile's K (non-persistent grid)
+  int a_mc = 1;       // A-multicast configs: CTAs per cluster sharing A (tiles (tm, a_mc * tg + r))
   int cluster_size() const { return cluster ? cluster : cta_group; }
 };
 
@@ -72,7 +78,8 @@ template <class C32, class C16>
 constexpr ConfigDesc make_desc() {
   return ConfigDesc{C32::CG, C32::BN, C32::STAGES, C32::THREADS, C32::BK,
                     {C32::SMEM_BYTES, C16::SMEM_BYTES}, {C32::CW, C16::CW}, {C32::RB, C16::RB},
-                    {&gemm_f16_sm100_kernel<C32>, &gemm_f16_sm100_kernel<C16>}};
+                    {&gemm_f16_sm100_kernel<C32>, &gemm_f16_sm100_kernel<C16>},
+                    C32::MC > 1 ? C32::MC : 0, 0, C32::MC};
 }
 
 template <int BN, int S>
@@ -98,6 +105,8 @@ const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
     make_splitk_desc<256, 2>(),
     make_splitk_desc<256, 4>(),
     make_splitk_desc<128, 4>(),
+    make_desc<Cfg13F32, Cfg13F16>(),
+    make_desc<Cfg14F32, Cfg14F16>(),
 };
 using CfgW16 = WCfg<4>;
 const ConfigDesc kWideConfig{2, CfgW16::BN, CfgW16::STAGES, CfgW16::THREADS, CfgW16::BK,
@@ -308,6 +317,9 @@ int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
     if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
     return GEMM_CFG_SOLO_128x64;
   }
+  // at most half a wave of pair tiles: 128 x 128 tiles keep twice as many SMs busy
+  // (2048 x 1024 x 1024: 9.2-10.5 us vs 12-13 us for the pair tile; profiles/r01/multicast.md)
+  if (2 * pair_tiles <= sm_count / 2 && cdiv(M, 128) * cdiv(N, 128) <= sm_count) return GEMM_CFG_SOLO_128x128;
   if (acc_type == GEMM_ACC_F32 && K <= 2048) return GEMM_CFG_PAIR_256x256_S5;
   if (acc_type == GEMM_ACC_F16) {
     // the 256 x 512 tile runs 5-10 % faster per wave under the power cap
@@ -385,7 +397,8 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (bias && !aligned16(bias)) return GEMM_ERR_MISALIGNED;
   CUtensorMap tm_a, tm_b, tm_c;
   const bool ok =
-      encode_2d(&tm_a, in_dt, 2, A, M, K, lda, 64, 128, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
+      encode_2d(&tm_a, in_dt, 2, A, M, K, lda, 64, static_cast<uint32_t>(128 / cd.a_mc),
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
       encode_2d(&tm_b, in_dt, 2, B, K, N, ldb, 64, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
       encode_2d(&tm_c, acc_type == GEMM_ACC_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                 acc_type == GEMM_ACC_F32 ? 4 : 2, C, M, N, ldc, static_cast<uint32_t>(cd.c_box_cols[a]), 32,
@@ -421,7 +434,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const int tile_m = 128 * cd.cta_group;
   const int cl_size = cd.cluster_size();
   p.tiles_m = static_cast<int>(cdiv(M, tile_m));
-  p.tiles_n = static_cast<int>(cdiv(N, cd.tile_n));
+  p.tiles_n = static_cast<int>(cdiv(cdiv(N, cd.tile_n), cd.a_mc));   // (A multicast: groups of a_mc tiles)
   const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n;
   if (tiles * std::max(1, cd.cluster_size()) > 0x7fffffffLL) return GEMM_ERR_INVALID_VALUE;
   p.num_tiles = static_cast<int>(tiles);

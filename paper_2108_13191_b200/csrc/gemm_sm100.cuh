@@ -92,9 +92,12 @@ struct GemmParams {
                                     //  C evict_first: streamed once)
 };
 
-template <int CG_, int BN_, int STAGES_, bool OUT_F16_, int EPI_SLOTS_ = 1, int BK_ = 64, bool PEERS_ = false>
+template <int CG_, int BN_, int STAGES_, bool OUT_F16_, int EPI_SLOTS_ = 1, int BK_ = 64, bool PEERS_ = false,
+          int MC_ = 1>
 struct KCfg {
   static constexpr int CG = CG_;            // CTAs per MMA (cta_group)
+  static constexpr int MC = MC_;            // cta_group::1 only: CTAs per cluster sharing (multicasting) A
+  static_assert(MC == 1 || (CG == 1 && (MC == 2 || MC == 4)), "A multicast: 1-CTA tiles, 2 or 4 per cluster");
   static constexpr int BN = BN_;            // UMMA N (tile columns)
   static constexpr int STAGES = STAGES_;
   static constexpr bool OUT_F16 = OUT_F16_;
@@ -217,7 +220,11 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const uint32_t lane = threadIdx.x & 31;
   if (p.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) p.trace[8 * 62 + 0] = globaltimer_ns();
+  constexpr int MC = Cfg::MC;
   const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+  // A multicast (MC > 1): the MC CTAs of a cluster own tiles (tm, MC * tg + r), r = rank
+  // in the cluster; each loads 128 / MC rows of the shared A box and multicasts them
+  const uint32_t mrank = (MC > 1) ? cluster_ctarank() : 0u;
 
   if (warp == Cfg::W_PRODUCER && lane == 0) {
     prefetch_tmap(&tm_a);
@@ -229,7 +236,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   if (warp == Cfg::W_MMA && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar + 8 * s, 1);
-      mbar_init(empty_bar + 8 * s, 1);
+      mbar_init(empty_bar + 8 * s, MC);   // MC > 1: a stage is refilled once every CTA's MMAs used it
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(accf_bar + 8 * b, 1);
@@ -240,7 +247,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   }
   if (warp == Cfg::W_ALLOC) tmem_alloc<CG>(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if constexpr (CG == 2 || MC > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   uint32_t tmem_base;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot) : "memory");
@@ -250,8 +257,8 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   griddep_wait();
   if (p.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) p.trace[8 * 62 + 1] = globaltimer_ns();
 
-  const int cluster = static_cast<int>(blockIdx.x) / CG;
-  const int nclusters = static_cast<int>(gridDim.x) / CG;
+  const int cluster = static_cast<int>(blockIdx.x) / (CG * MC);
+  const int nclusters = static_cast<int>(gridDim.x) / (CG * MC);
 
   if (warp == Cfg::W_PRODUCER) {
     // ===================== TMA producer =====================
@@ -265,6 +272,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
         int tm, tn;
         tile_coords(tile, p, tm, tn);
+        if constexpr (MC > 1) tn = MC * tn + static_cast<int>(mrank);
         const int a_row = tm * BM * CG + static_cast<int>(rank) * BM;
         const int b_col = tn * BN + static_cast<int>(rank) * Cfg::BN_CTA;
         const bool backwards = p.k_serpentine && (it & 1);
@@ -303,6 +311,14 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
               for (int h = 0; h < Cfg::BN_CTA / 64; ++h)
                 tma_load_2d_pair_hint(b_dst + kh * Cfg::B_HALF_BYTES + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h,
                                       kc, fb, pol_b);
+            } else if constexpr (MC > 1) {
+              // this CTA's 128 / MC rows of A, multicast into every CTA of the cluster
+              tma_load_2d_mc_hint(a_dst + kh * Cfg::A_HALF_BYTES + mrank * (Cfg::A_HALF_BYTES / MC), &tm_a, kc,
+                                  a_row + static_cast<int>(mrank) * (BM / MC), fb, (1u << MC) - 1u, pol_a);
+#pragma unroll
+              for (int h = 0; h < Cfg::BN_CTA / 64; ++h)
+                tma_load_2d_hint(b_dst + kh * Cfg::B_HALF_BYTES + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h, kc,
+                                 fb, pol_b);
             } else {
               tma_load_2d_hint(a_dst + kh * Cfg::A_HALF_BYTES, &tm_a, kc, a_row, fb, pol_a);
 #pragma unroll
@@ -355,6 +371,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
               umma_f16<CG>(d_tmem, adesc, bdesc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             }
             if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, 0x3);
+            else if constexpr (MC > 1) umma_commit_mc(empty_bar + 8 * stage, (1u << MC) - 1u);   // every CTA's stage
             else umma_commit(empty_bar + 8 * stage);
             if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
           }
@@ -389,6 +406,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       const bool tr = p.trace != nullptr && blockIdx.x == 0 && ew == 0 && lane == 0 && it < 60;
       int tm, tn;
       tile_coords(tile, p, tm, tn);
+      if constexpr (MC > 1) tn = MC * tn + static_cast<int>(mrank);
       const int row0 = tm * BM * CG + static_cast<int>(rank) * BM + static_cast<int>(q) * 32;
       const int col0 = tn * BN + static_cast<int>(hcol);
       if (tr) p.trace[8 * it + 3] = globaltimer_ns();
@@ -568,7 +586,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   // ===================== teardown =====================
   __syncwarp();
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if constexpr (CG == 2 || MC > 1) cluster_sync(); else __syncthreads();   // (no peer arrives on our barriers any more)
   if (warp == Cfg::W_ALLOC) {
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, Cfg::TMEM_COLS);

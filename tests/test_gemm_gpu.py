@@ -14,7 +14,8 @@ from parity import Guarded, check, device_problem, oracle_full, round_up, stats
 
 pytestmark = pytest.mark.gpu
 
-CFGS = ["pair_256x256", "pair_256x128", "solo_128x256", "solo_128x128", "solo_128x64"]
+CFGS = ["pair_256x256", "pair_256x128", "solo_128x256", "solo_128x128", "solo_128x64", "solo_128x64_mc4",
+        "solo_128x128_mc4"]
 
 
 @pytest.fixture(scope="module")
@@ -299,6 +300,24 @@ def test_host_path_resident_operands(g, M):
     g.gemm_f16_host(torch.from_numpy(A2).pin_memory(), None, hC16b, dA, dB, dC16, stream=s)
     s.synchronize()
     check(hC16b.numpy(), oracle_full(A2, B, C16)[0], A2, B, "f16", K, "host, B resident")
+
+
+@pytest.mark.parametrize("cfg", ["solo_128x64_mc4", "solo_128x128_mc4"])
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+@pytest.mark.parametrize("shape", [(1024, 1024, 1024), (130, 70, 200), (300, 1000, 777), (129, 640, 64), (1, 1, 1)])
+def test_a_multicast_configs(g, cfg, acc, shape):
+    """4-CTA clusters share A by TMA multicast: each CTA loads a quarter of the A box
+    for all four.  Cases: N tiles not a multiple of 4 (CTAs whose tile lies wholly
+    outside C still load their quarter of A and must write nothing), one cluster
+    walking all tiles (phase wrap), ragged K, guard bands."""
+    M, N, K = shape
+    A, B, C, gA, gB, gC = device_problem(M, N, K, acc, seed=M + K, pad=(8, 8, 8))
+    for mc in (0, 1):
+        gC.full.copy_(__import__("torch").from_numpy(gC.full_host.copy()))
+        _run(g, gA, gB, gC, config=cfg, max_clusters=mc)
+        ex, _ = oracle_full(A, B, C)
+        check(gC.result(), ex, A, B, acc, K, f"{cfg} {acc} {shape} clusters={mc}")
+        assert gC.guard_intact(), "write outside the M x N window"
 
 
 def test_cuda_graph_capture_replay(g):
