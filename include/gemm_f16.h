@@ -126,6 +126,10 @@ typedef struct {
   int raster;       /* 0: default; 1: serpentine raster -- odd groups of group_m tile-rows */
                     /* walk their column strips right to left, so the B columns the last  */
                     /* wave of a group used are the first the next group needs; -1: plain */
+  int c_reduce;     /* F32 C, plain C += A.B (no bias/ReLU, N % 4 == 0): 1 = the epilogue   */
+                    /* adds its tile into C with a TMA reduce-add store instead of loading */
+                    /* C_in into shared memory (bitwise the same single RN add); -1 = off; */
+                    /* 0 = default (on)                                                     */
 } gemm_options_t;
 
 /*

@@ -30,6 +30,7 @@ constexpr unsigned kDefaultWaitHintNs = 0;
 constexpr int kDefaultCRowPrefetch = 0;
 constexpr int kDefaultPdl = 1;   // profiles/r01/findings.md section 9
 constexpr int kDefaultSnake = 0;
+constexpr int kDefaultCReduce = 1;   // findings.md section 14: +1-10 %, bitwise identical
 
 thread_local int t_last_cuda_error = 0;
 thread_local int t_last_launches = 0;
@@ -507,6 +508,9 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const int raster = opts ? opts->raster : 0;
   if (raster < -1 || raster > 1) return GEMM_ERR_INVALID_VALUE;
   p.snake = raster == 0 ? kDefaultSnake : (raster > 0 ? 1 : 0);
+  const int cred = opts ? opts->c_reduce : 0;
+  if (cred < -1 || cred > 1) return GEMM_ERR_INVALID_VALUE;
+  p.c_reduce = cred == 0 ? kDefaultCReduce : (cred > 0 ? 1 : 0);
   const int pdl_opt = opts ? opts->pdl : 0;
   if (pdl_opt < -1 || pdl_opt > 1) return GEMM_ERR_INVALID_VALUE;
   if (pdl_opt == 0 ? kDefaultPdl : pdl_opt > 0) {

@@ -56,6 +56,7 @@ struct GemmParams {
                                     // each accumulating a contiguous share of the k-blocks
   int group_m;                      // raster group height in tiles
   int snake;                        // 1: odd raster groups walk their columns right to left
+  int c_reduce;                     // 1: F32 C += acc by TMA reduce-add (C_in never staged; see epilogue)
   int c_ragged;                     // N * sizeof(C) % 16 != 0: TMA stores would write a
                                     // whole 16-byte granule past column N-1, so the chunk
                                     // holding column N-1 is stored element-wise instead
@@ -395,7 +396,13 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     const uint32_t acce_leader = (CG == 2) ? mapa_shared(acce_bar, 0) : acce_bar;
     const uint64_t pol_c = p.l2_hints ? policy_evict_first() : policy_evict_normal();
     const bool no_c = (p.debug_flags & 2) != 0;
-    const bool load_c = !no_c && !p.beta0;   // C_in traffic (beta = 1)
+    // F32 C, plain C += A.B: the staged accumulator is added into C by the TMA unit
+    // (cp.reduce.async.bulk .add, one IEEE RN add in L2 -- bitwise the same C_in + acc),
+    // so C_in is never loaded into shared memory: half the epilogue's shared-memory
+    // traffic and no C_in latency chain (findings.md section 14)
+    const bool red = !Cfg::OUT_F16 && !Cfg::PEERS && !no_c && !p.beta0 && p.c_reduce && p.bias == nullptr &&
+                     !p.relu && !p.c_ragged;
+    const bool load_c = !no_c && !p.beta0 && !red;   // C_in traffic through the staging slots
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t slot_phase = 0;  // bit s = parity to wait for on slot s
@@ -501,8 +508,9 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           constexpr int EPU = 16 / Cfg::ESIZE;      // output elements per 16-byte unit
           float o[EPU];
           if constexpr (!Cfg::OUT_F16) {
-            float4 ci = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (!p.beta0) ci = lds128(addr);
+            const float z = red ? -0.f : 0.f;   // (reduce-add: stage the accumulator itself, -0 kept)
+            float4 ci = make_float4(z, z, z, z);
+            if (load_c) ci = lds128(addr);
             o[0] = ci.x + a[0]; o[1] = ci.y + a[1]; o[2] = ci.z + a[2]; o[3] = ci.w + a[3];
           } else {
             uint4 ci = make_uint4(0u, 0u, 0u, 0u);
@@ -534,7 +542,8 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d_hint(&tm_c, ccol, row0, sbuf, pol_c);
+            if (red) tma_reduce_add_2d_hint(&tm_c, ccol, row0, sbuf, pol_c);
+            else tma_store_2d_hint(&tm_c, ccol, row0, sbuf, pol_c);
             // fused all-gather: the same staged chunk goes to every peer's C
             if constexpr (Cfg::PEERS)
               for (int d = 0; d < p.n_peers; ++d) tma_store_2d_hint(&peers.m[d], ccol, row0, sbuf, pol_c);

@@ -128,6 +128,14 @@ __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* m, int32_t 
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;"
                :: "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(src), "l"(policy) : "memory");
 }
+// 2-D TMA reduce-add store: global[box] += smem tile, element type from the tensor map
+// (F32: the L2 performs one IEEE round-to-nearest add per element), bulk_group completion.
+__device__ __forceinline__ void tma_reduce_add_2d_hint(const CUtensorMap* m, int32_t c0, int32_t c1, uint32_t src,
+                                                       uint64_t policy) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;"
+      :: "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(src), "l"(policy) : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));

@@ -233,7 +233,8 @@ def test_promotion_bounds_long_k_error(g):
 
 @pytest.mark.parametrize("kw", [
     {"ring_stages": 1}, {"ring_stages": 2}, {"acc_bufs": 1}, {"acc_bufs": 1, "ring_stages": 1},
-    {"group_m": 1}, {"group_m": 3}, {"raster": 1}, {"raster": 1, "group_m": 2}, {"l2_hints": -1}, {"epi_pace": -1},
+    {"group_m": 1}, {"group_m": 3}, {"raster": 1}, {"raster": 1, "group_m": 2}, {"c_reduce": 1}, {"c_reduce": -1},
+    {"c_reduce": 1, "config": "pair_256x256_s5"}, {"c_reduce": 1, "config": "solo_128x64"}, {"l2_hints": -1}, {"epi_pace": -1},
     {"max_clusters": 1000},
     {"config": "pair_256x256_s5"}, {"config": "pair_256x256_s4"}, {"config": "solo_128x256", "ring_stages": 1, "acc_bufs": 1},
     {"k_serpentine": 1, "max_clusters": 2}, {"wait_hint_ns": 20000}, {"epi_pace": 1},
@@ -318,6 +319,32 @@ def test_a_multicast_configs(g, cfg, acc, shape):
         ex, _ = oracle_full(A, B, C)
         check(gC.result(), ex, A, B, acc, K, f"{cfg} {acc} {shape} clusters={mc}")
         assert gC.guard_intact(), "write outside the M x N window"
+
+
+@pytest.mark.parametrize("cfg", ["pair_256x256_s5", "pair_256x256_k128", "pair_256x256", "solo_128x64",
+                                 "solo_128x64_mc4"])
+def test_c_reduce_bitwise_equal_to_staged(g, cfg):
+    """F32 C by TMA reduce-add (c_reduce): the L2 adds the staged accumulator into C_in
+    -- the same single IEEE RN add as the staged path, so the results must be bitwise
+    equal, on a ragged, padded, guard-banded problem whose C_in holds -0.0, +-Inf, NaN
+    and subnormals too."""
+    import torch
+    M, N, K = 777, 1000, 1000                      # N % 4 == 0: reduce-add applies
+    A, B, C, gA, gB, gC = device_problem(M, N, K, "f32", seed=13, pad=(8, 8, 4))
+    C = C.copy()
+    C[::7, ::5] = -0.0
+    C[3, :8] = [np.inf, -np.inf, np.nan, 1e-40, -1e-40, 3.4e38, -3.4e38, 0.0]
+    base = Guarded(C, gC.ld)
+    outs = []
+    for red in (1, -1):
+        gC.full.copy_(torch.from_numpy(base.full_host.copy()))
+        _run(g, gA, gB, gC, config=cfg, c_reduce=red)
+        outs.append(gC.result().copy())
+        assert gC.guard_intact()
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    finite = np.isfinite(C).all(axis=1)
+    ex, _ = oracle_full(A, B, C)
+    check(outs[0][finite], ex[finite], A[finite], B, "f32", K, f"c_reduce {cfg}")
 
 
 def test_cuda_graph_capture_replay(g):
