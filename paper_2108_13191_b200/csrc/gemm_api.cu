@@ -291,7 +291,8 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 //  * 128-deep K stages (3 x 64 KB) beat 64-deep ones (6 x 32 KB) by 2-4 %:
 //    half the barrier/commit round trips per FLOP and fewer DRAM re-reads;
 //  * for F32 C with one K chunk per tile (K <= 2048) the tile is bound by its C
-//    traffic, and a second epilogue staging slot per warp (5 x 32 KB ring) wins;
+//    traffic: with C_in staged a second epilogue staging slot per warp (5 x 32 KB ring)
+//    won; with the reduce-add epilogue the 6-stage ring does;
 //  * when the whole problem is under a third of a wave of pair tiles
 //    (e.g. 1024^3), fixed per-tile latency dominates and the 1-CTA 128x64 tile
 //    (more, shorter tiles) wins (GPU time from CUDA-graph replay);
@@ -321,7 +322,10 @@ int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
   // at most half a wave of pair tiles: 128 x 128 tiles keep twice as many SMs busy
   // (2048 x 1024 x 1024: 9.2-10.5 us vs 12-13 us for the pair tile; profiles/r01/multicast.md)
   if (2 * pair_tiles <= sm_count / 2 && cdiv(M, 128) * cdiv(N, 128) <= sm_count) return GEMM_CFG_SOLO_128x128;
-  if (acc_type == GEMM_ACC_F32 && K <= 2048) return GEMM_CFG_PAIR_256x256_S5;
+  // F32 C with one K chunk: with the reduce-add epilogue (N % 4 == 0) C_in needs no
+  // staging slot, and the 6-stage 64-deep ring is best (profiles/r01/f32_short_k_cfg.txt);
+  // a ragged N still stages C_in and keeps the second slot of S5
+  if (acc_type == GEMM_ACC_F32 && K <= 2048) return N % 4 == 0 ? GEMM_CFG_PAIR_256x256 : GEMM_CFG_PAIR_256x256_S5;
   if (acc_type == GEMM_ACC_F16) {
     // the 256 x 512 tile runs 5-10 % faster per wave under the power cap
     // (profiles/r01/wide_tile.md) but has half as many tiles: take it unless it
