@@ -6,8 +6,10 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 import torch, synth
 import paper_2108_13191_b200 as g
 
-PEAK_TF = 1611.6
-HBM = 6545.9e9
+_mp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "MEASURED_PEAKS.json")
+_peaks = json.load(open(_mp)) if os.path.exists(_mp) else {}
+PEAK_TF = float(_peaks.get("bf16_tflops", 1611.6))   # fp16 dense = bf16 rate (nominal 1:1)
+HBM = float(_peaks.get("hbm_gbs", 6545.9)) * 1e9
 shapes = [(1024, 1024, 1024)] + [(s, s, s) for s in range(2048, 16385, 2048)]
 shapes += [(4096, 1024, 1024), (4096, 1024, 4096), (4096, 4096, 1024), (4096, 4096, 4096), (8192, 1024, 1024),
            (8192, 1024, 4096), (8192, 4096, 1024), (8192, 4096, 4096), (16384, 1024, 1024), (16384, 1024, 4096),
