@@ -329,6 +329,7 @@ def main():
     peaks = load_peaks()
     mode_stats = {m: {"tflops": flops / (per_mode_ms[m] * 1e-3) / 1e12, "ms": per_mode_ms[m],
                       "frac_of_2250": flops / (per_mode_ms[m] * 1e-3) / 1e12 / NOMINAL_F16_DENSE_TFLOPS,
+                      "frac_of_measured_peak": flops / (per_mode_ms[m] * 1e-3) / 1e12 / peaks["tflops"],
                       "config": g.pick_config(M, N, K, 0 if m == "f32" else 1) if args.config == "auto"
                       else g.CONFIGS[args.config]} for m in modes}
     dom = max(modes, key=lambda m: per_mode_ms[m])
