@@ -311,7 +311,7 @@ int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
     // DSMEM reduction (profiles/r01/splitk.md; it loses at K <= 2048 with 1024^2)
     // Each CTA keeps one truncating TMEM chain over its K / S (no promotion, R4):
     // for F32 C that chain stays <= 4096 long (rel. error <~ 5e-6, bar 1e-5).
-    const int64_t kmax_chain = acc_type == GEMM_ACC_F32 ? 4096 : INT64_MAX;
+    const int64_t kmax_chain = acc_type == GEMM_ACC_F32 ? 4096 : (int64_t(1) << 40);   // (F16: no limit)
     const int64_t t128 = cdiv(M, 128) * cdiv(N, 128), t256 = cdiv(M, 128) * cdiv(N, 256);
     if (K >= 2048 && 4 * t128 <= sm_count && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x128_S4;
     if (K >= 8192 && 4 * t256 <= sm_count && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S4;
@@ -406,7 +406,8 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
       encode_2d(&tm_b, in_dt, 2, B, K, N, ldb, 64, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
       encode_2d(&tm_c, acc_type == GEMM_ACC_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                acc_type == GEMM_ACC_F32 ? 4 : 2, C, M, N, ldc, static_cast<uint32_t>(cd.c_box_cols[a]), 32,
+                acc_type == GEMM_ACC_F32 ? 4 : 2, C, M, N, ldc, static_cast<uint32_t>(cd.c_box_cols[a]),
+                cd.k_splits ? 128 : 32,   // split-K: whole 128-row boxes for the reduce-add steps
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 cd.c_row_bytes[a] == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return cuda_fail(cudaErrorInvalidValue);

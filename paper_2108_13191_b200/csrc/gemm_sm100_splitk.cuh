@@ -79,7 +79,7 @@ template <class Cfg>
 __global__ void __launch_bounds__(192, 1)
 gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
                              const __grid_constant__ CUtensorMap tm_b,
-                             const __grid_constant__ CUtensorMap /*tm_c: unused*/,
+                             const __grid_constant__ CUtensorMap tm_c,   // C, box 32 x 128, 128B swizzle (reduce-add path)
                              const __grid_constant__ GemmParams p,
                              const __grid_constant__ PeerMaps /*unused*/,
                              const __grid_constant__ CUtensorMap tm_cin) {   // C, box CW x 128, no swizzle
@@ -184,6 +184,53 @@ gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
   cluster_sync();
   tc_fence_after();
   if (tr) p.trace[3] = globaltimer_ns();
+  // F32 C, plain C += A.B: no DSMEM exchange at all.  Each CTA stages its whole partial
+  // (128B-swizzled 32-column boxes) and the TMA unit adds it into C (reduce-add, one RN
+  // add in L2), one column slice per step in a rotation -- in step j CTA r adds slice
+  // (r + j) % S -- with a cluster barrier between steps, so every element receives
+  // C_in + p_s + p_(s-1) + ... in a fixed order (deterministic).
+  const bool red = !Cfg::OUT_F16 && load_c && p.c_reduce && p.bias == nullptr && !p.relu && !p.c_ragged;
+  if (red) {
+    if (warp < 4) {
+      const uint32_t row = warp * 32 + lane;
+      const uint32_t t_row = tmem_base + ((warp * 32u) << 16);
+      const bool empty_share = kb1 <= kb0;   // -0 is the additive identity for every x
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + 32 * c, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float x = __uint_as_float(v[j]);
+          if (p.accum_f16) x = f16x2_to_f32(v[j]).x;
+          v[j] = __float_as_uint(empty_share ? -0.f : x);
+        }
+        const uint32_t box = sR + static_cast<uint32_t>(c) * (BM * 128);   // 128 rows x 128 B
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          sts128u(box + swz<128>(row, static_cast<uint32_t>(j)), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+      fence_proxy_async_smem();
+    }
+    __syncthreads();
+    if (tr) p.trace[4] = globaltimer_ns();
+#pragma unroll 1
+    for (int j = 0; j < S; ++j) {
+      if (threadIdx.x == 0) {
+        const int sl = (static_cast<int>(r) + j) % S;
+#pragma unroll 1
+        for (int b = sl * (CW / 32); b < (sl + 1) * (CW / 32); ++b)
+          tma_reduce_add_2d_hint(&tm_c, tn * BN + 32 * b, tm * BM, sR + static_cast<uint32_t>(b) * (BM * 128),
+                                 policy_evict_first());
+        bulk_commit_group();
+        bulk_wait_group<0>();   // this step's adds are performed before the barrier
+      }
+      __syncwarp();
+      cluster_sync();
+    }
+    if (tr) p.trace[5] = globaltimer_ns();
+  } else {
   if (warp == Cfg::W_PRODUCER && lane == 0 && load_c) {
     mbar_arrive_expect_tx(cin_bar, Cfg::CIN_BYTES);
     tma_load_2d_hint(sC, &tm_cin, tn * BN + static_cast<int>(r) * CW, tm * BM, cin_bar, policy_evict_first());
@@ -274,6 +321,7 @@ gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
       }
     }
   }
+  }   // DSMEM path
   __syncwarp();
   if (tr) p.trace[6] = globaltimer_ns();
   if (warp == Cfg::W_MMA) {

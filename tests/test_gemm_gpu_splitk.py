@@ -157,6 +157,7 @@ def test_splitk_auto_long_k_accuracy(g, shape):
     import torch
     M, N, K = shape
     assert g.pick_config(M, N, K, g.ACC_F32) in (10, 11, 12)
+    assert g.pick_config(M, N, K, g.ACC_F16) in (10, 11, 12)
     for acc in ("f32", "f16"):
         A, B, C = synth.problem(M, N, K, acc, seed=11)
         dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
