@@ -73,7 +73,8 @@ def test_error_vs_k_matches_model(K):
     C0 = np.zeros_like(C)
     rows = np.arange(0, M, 8)
     ex, _ = oracle.gemm(A, B, C0, rows=rows)
-    one_chain = stats(_run(A, B, C0, promote_k=-1)[rows], ex)["rel_fro"]
+    # one TMEM chain over all of K (auto would split K over a cluster for this small output)
+    one_chain = stats(_run(A, B, C0, promote_k=-1, config="pair_256x256")[rows], ex)["rel_fro"]
     assert MODEL[K] / 1.5 <= one_chain <= MODEL[K] * 1.5, one_chain
     promoted = stats(_run(A, B, C0, promote_k=512, config="pair_256x256")[rows], ex)["rel_fro"]
     assert promoted <= F16_FRO, promoted          # promotion every 512 keeps the BASELINE bar
