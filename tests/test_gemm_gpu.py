@@ -347,6 +347,37 @@ def test_c_reduce_bitwise_equal_to_staged(g, cfg):
     check(outs[0][finite], ex[finite], A[finite], B, "f32", K, f"c_reduce {cfg}")
 
 
+def test_pdl_mixed_kernel_chain_exact(g):
+    """The bench's launch pattern under PDL: different kernels back to back on one stream
+    (F32 pair tile with the reduce-add epilogue, F16 256x512 tile, split-K, 1-CTA), each
+    reading what an earlier one wrote, so every kernel's prologue overlaps a different
+    kernel's tail.  Small-integer inputs make every result exact."""
+    import torch
+    rng = np.random.default_rng(17)
+    M, N, K = 512, 1024, 2048
+    A = torch.from_numpy(rng.integers(-1, 2, (M, K)).astype(np.float16)).cuda()
+    B = torch.from_numpy(rng.integers(-1, 2, (K, N)).astype(np.float16)).cuda()
+    C32 = torch.from_numpy(rng.integers(-40, 41, (M, N)).astype(np.float32)).cuda()
+    C16 = torch.from_numpy(rng.integers(-40, 41, (M, N)).astype(np.float16)).cuda()
+    AB = (A.double() @ B.double())
+    want32 = C32.double().clone()
+    want16 = C16.double().clone()
+    seq = [("f32", "pair_256x256_k128"), ("f16", "pair_256x512"), ("f32", "splitk_128x128_s4"),
+           ("f16", "pair_256x512"), ("f32", "solo_128x64"), ("f16", "splitk_128x256_s2"), ("f32", "pair_256x256")]
+    for _ in range(2):
+        for mode, cfg in seq:
+            if mode == "f32":
+                g.gemm_f16(A, B, C32, config=cfg, pdl=1)
+                want32 += AB
+            else:
+                g.gemm_f16(A, B, C16, config=cfg, pdl=1)
+                want16 += AB
+    torch.cuda.synchronize()
+    assert float(want16.abs().max()) <= 2048          # every F16 result exact
+    assert torch.equal(C32.double(), want32)
+    assert torch.equal(C16.double(), want16)
+
+
 def test_cuda_graph_capture_replay(g):
     """The C ABI is capturable: gemm_f16 calls recorded into a CUDA graph replay
     to the same results as eager calls (tensor maps travel as kernel params)."""
