@@ -26,7 +26,11 @@
  * (asynchronous with respect to the host); kernel faults surface at the
  * caller's next synchronisation, as usual in CUDA.  Reentrant and thread-safe.
  * Results are bitwise reproducible for identical inputs, shape, mode and
- * options on the same device model (no split-K, no atomics).
+ * options on the same device model: every element's sum has a fixed order.
+ * The F32 epilogue adds the tile into C with a TMA reduce-add, one writer per
+ * element.  The split-K configurations combine their partial sums in a fixed
+ * order, through distributed shared memory or in reduce-add steps separated
+ * by cluster barriers.  No atomics race.
  */
 #ifndef GEMM_F16_H_
 #define GEMM_F16_H_
