@@ -277,6 +277,14 @@ __device__ __forceinline__ void st_async_v4(uint32_t cluster_addr, uint32_t a, u
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
                :: "r"(cluster_addr), "r"(a), "r"(b), "r"(c), "r"(d), "r"(cluster_bar) : "memory");
 }
+// Bulk DMA copy from this CTA's shared memory into another CTA's shared memory
+// (cluster addresses from mapa_shared), `bytes` (multiple of 16) counted on that
+// CTA's mbarrier `cluster_bar`.
+__device__ __forceinline__ void bulk_copy_s2dsmem(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
+                                                  uint32_t cluster_bar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst_cluster), "r"(src_cta), "r"(bytes), "r"(cluster_bar) : "memory");
+}
 // Plain 16-byte store into the shared memory of a CTA of the cluster (address from
 // mapa_shared); made visible to that CTA by the next cluster barrier (release/acquire).
 __device__ __forceinline__ void st_cluster_v4(uint32_t cluster_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
