@@ -12,7 +12,10 @@
 // through distributed shared memory, with no workspace and no atomics:
 //   1. cluster barrier: every CTA's mainloop is done, so the operand rings are idle;
 //   2. CTA r owns columns [r BN / S, (r+1) BN / S) of the tile.  Every CTA reads its
-//      partial out of TMEM and pushes each owner's columns into slot r of that
+//      partial out of TMEM.  Where everything fits in the idle ring (SKCfg::DMA,
+//      S4 x 128x128) it stages the partial slot-major and sends each owner its slot
+//      with one bulk DMA copy (cp.async.bulk.shared::cluster, counted on the owner's
+//      mbarrier).  Otherwise it pushes each owner's columns into slot r of that
 //      owner's receive buffer with plain 16-byte st.shared::cluster stores
 //      (fire-and-forget; an st.async per 16 bytes, each updating the owner's
 //      mbarrier, measured ~15 us for 128 KB); meanwhile one thread TMA-loads the
@@ -58,8 +61,14 @@ struct SKCfg {
   static constexpr int OFF_CIN = S * SLOT_BYTES;         // C_in slice, TMA-loaded
   static constexpr int CIN_BYTES = BM * CW * ESIZE;
   static_assert(OFF_CIN + CIN_BYTES <= RING_BYTES, "receive buffer + C_in must fit in the operand ring");
+  // DSMEM exchange by bulk DMA where the own partial (S slots), the S-1 received slots
+  // and the C_in slice all fit in the idle ring (S4 x 128x128): one
+  // cp.async.bulk.shared::cluster copy per peer instead of 16-byte remote stores
+  static constexpr bool DMA = (2 * S - 1) * SLOT_BYTES + CIN_BYTES <= RING_BYTES;
+  static constexpr int OFF_RECV_DMA = S * SLOT_BYTES;
+  static constexpr int OFF_CIN_DMA = (2 * S - 1) * SLOT_BYTES;
   static constexpr int OFF_BAR = RING_BYTES;
-  static constexpr int NBAR = 2 * STAGES + 2;            // full[S], empty[S], acc_full, cin
+  static constexpr int NBAR = 2 * STAGES + 3;            // full[S], empty[S], acc_full, cin, recv
   static constexpr int SMEM_BYTES = 1024 + OFF_BAR + NBAR * 8 + 16;
   static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of dynamic shared memory");
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
@@ -96,6 +105,7 @@ gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
   const uint32_t empty_bar = bar0 + 8 * STAGES;
   const uint32_t accf_bar = bar0 + 16 * STAGES;
   const uint32_t cin_bar = accf_bar + 8;
+  const uint32_t recv_bar = accf_bar + 16;   // (DMA exchange)
   const uint32_t tmem_slot = bar0 + 8 * Cfg::NBAR;
 
   const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
@@ -121,7 +131,10 @@ gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
     }
     mbar_init(accf_bar, 1);
     mbar_init(cin_bar, 1);
+    mbar_init(recv_bar, 1);
     fence_mbarrier_init();
+    // armed before any peer can send (sends start after the second cluster barrier)
+    if constexpr (Cfg::DMA) mbar_arrive_expect_tx(recv_bar, (S - 1) * Cfg::SLOT_BYTES);
   }
   if (warp == Cfg::W_MMA) tmem_alloc<1>(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
@@ -230,6 +243,112 @@ gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
       cluster_sync();
     }
     if (tr) p.trace[5] = globaltimer_ns();
+  } else if constexpr (Cfg::DMA) {
+    const uint32_t sStage = base;                         // own partial, slot-major by owner
+    const uint32_t sRecv = base + Cfg::OFF_RECV_DMA;      // S-1 slots from the peers
+    const uint32_t sCin = base + Cfg::OFF_CIN_DMA;        // this CTA's C_in slice
+    if (warp == Cfg::W_PRODUCER && lane == 0 && load_c) {
+      mbar_arrive_expect_tx(cin_bar, Cfg::CIN_BYTES);
+      tma_load_2d_hint(sCin, &tm_cin, tn * BN + static_cast<int>(r) * CW, tm * BM, cin_bar, policy_evict_first());
+    }
+    if (warp < 4) {
+      const uint32_t row = warp * 32 + lane;
+      const uint32_t t_row = tmem_base + ((warp * 32u) << 16);
+      const bool empty_share = kb1 <= kb0;   // this CTA accumulated nothing: its partial is 0
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + 32 * c, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float x = __uint_as_float(v[j]);
+          if (p.accum_f16) x = f16x2_to_f32(v[j]).x;
+          v[j] = __float_as_uint(empty_share ? 0.f : x);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int col = 32 * c + 4 * j;          // tile column of this 16-byte unit
+          const int sl = col / CW;                 // its owner (a constant after unrolling)
+          sts128u(sStage + sl * Cfg::SLOT_BYTES + slot_off<CW>(row, static_cast<uint32_t>(col % CW)), v[4 * j],
+                  v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+      }
+      fence_proxy_async_smem();   // generic writes before the bulk copies read them
+    }
+    __syncthreads();
+    if (tr) p.trace[4] = globaltimer_ns();
+    if (threadIdx.x == 0) {   // one bulk copy per peer: my slot s -> slot (r < s ? r : r - 1) of CTA s
+#pragma unroll 1
+      for (int sl = 0; sl < S; ++sl) {
+        if (sl == static_cast<int>(r)) continue;
+        const uint32_t slot = r < static_cast<uint32_t>(sl) ? r : r - 1u;
+        bulk_copy_s2dsmem(mapa_shared(sRecv + slot * Cfg::SLOT_BYTES, static_cast<uint32_t>(sl)),
+                          sStage + sl * Cfg::SLOT_BYTES, Cfg::SLOT_BYTES,
+                          mapa_shared(recv_bar, static_cast<uint32_t>(sl)));
+      }
+    }
+    if (warp < 4) {
+      mbar_wait(recv_bar, 0);
+      if (load_c) mbar_wait(cin_bar, 0);
+      if (tr) p.trace[5] = globaltimer_ns();
+#pragma unroll 4
+      for (int i = static_cast<int>(threadIdx.x); i < BM * U; i += 128) {
+        const int lr = i / U, lc = 4 * (i % U);
+        const int grow = tm * BM + lr, gcol = tn * BN + static_cast<int>(r) * CW + lc;
+        if (grow >= p.M || gcol >= p.N) continue;
+        const uint32_t off = slot_off<CW>(static_cast<uint32_t>(lr), static_cast<uint32_t>(lc));
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int sl = 0; sl < S; ++sl) {   // partials in the fixed order s = 0..S-1
+          const uint32_t src = sl == static_cast<int>(r)
+                                   ? sStage + sl * Cfg::SLOT_BYTES + off
+                                   : sRecv + static_cast<uint32_t>(sl < static_cast<int>(r) ? sl : sl - 1) *
+                                                 Cfg::SLOT_BYTES + off;
+          const float4 t = lds128(src);
+          if (sl == 0) acc = t;
+          else { acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w; }
+        }
+        float o[4] = {acc.x, acc.y, acc.z, acc.w};
+        if (load_c) {
+          const uint32_t coff = sCin + static_cast<uint32_t>((lr * CW + lc) * Cfg::ESIZE);
+          if constexpr (!Cfg::OUT_F16) {
+            const float4 ci = lds128(coff);
+            o[0] = ci.x + o[0]; o[1] = ci.y + o[1]; o[2] = ci.z + o[2]; o[3] = ci.w + o[3];
+          } else {
+            uint32_t lo, hi;
+            asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(coff));
+            const float2 a = f16x2_to_f32(lo), b = f16x2_to_f32(hi);
+            o[0] = a.x + o[0]; o[1] = a.y + o[1]; o[2] = b.x + o[2]; o[3] = b.y + o[3];
+          }
+        }
+        const int nv = min(4, p.N - gcol);           // valid columns of this unit
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (p.bias != nullptr && e < nv) o[e] += __ldg(p.bias + gcol + e);
+          if (p.relu) o[e] = relu_keep_nan(o[e]);
+        }
+        if constexpr (!Cfg::OUT_F16) {
+          float* cp = static_cast<float*>(p.c_ptr) + static_cast<long long>(grow) * p.ldc + gcol;
+          if (nv == 4) *reinterpret_cast<float4*>(cp) = make_float4(o[0], o[1], o[2], o[3]);
+          else for (int e = 0; e < nv; ++e) cp[e] = o[e];
+        } else {
+          uint16_t* cp = static_cast<uint16_t*>(p.c_ptr) + static_cast<long long>(grow) * p.ldc + gcol;
+          const uint32_t lo = cvt_f16x2_rn(o[0], o[1]), hi = cvt_f16x2_rn(o[2], o[3]);
+          if (nv == 4) {
+            *reinterpret_cast<uint2*>(cp) = make_uint2(lo, hi);
+          } else {
+            const uint16_t h[4] = {static_cast<uint16_t>(lo), static_cast<uint16_t>(lo >> 16),
+                                   static_cast<uint16_t>(hi), static_cast<uint16_t>(hi >> 16)};
+            for (int e = 0; e < nv; ++e) cp[e] = h[e];
+          }
+        }
+      }
+    }
+    // every copy into every CTA has landed (each owner waited) before any CTA exits:
+    // the copies read their senders' shared memory
+    __syncwarp();
+    cluster_sync();
   } else {
   if (warp == Cfg::W_PRODUCER && lane == 0 && load_c) {
     mbar_arrive_expect_tx(cin_bar, Cfg::CIN_BYTES);
