@@ -314,7 +314,10 @@ int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
     const int64_t kmax_chain = acc_type == GEMM_ACC_F32 ? 4096 : (int64_t(1) << 40);   // (F16: no limit)
     const int64_t t128 = cdiv(M, 128) * cdiv(N, 128), t256 = cdiv(M, 128) * cdiv(N, 256);
     if (K >= 2048 && 4 * t128 <= sm_count && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x128_S4;
-    if (K >= 8192 && 4 * t256 <= sm_count && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S4;
+    // (F32 reduces by TMA reduce-add and prefers S4 from K = 4096; F16 pushes through DSMEM,
+    //  where S2 wins at 1024^2 x 4096 and S4 at 1024^2 x 8192 -- splitk.md)
+    const int64_t k_s4 = acc_type == GEMM_ACC_F32 ? 4096 : 8192;
+    if (K >= k_s4 && 4 * t256 <= sm_count && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S4;
     if (K >= 4096 && 2 * t256 <= sm_count && K <= 2 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S2;
     if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
     return GEMM_CFG_SOLO_128x64;

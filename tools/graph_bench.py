@@ -6,6 +6,7 @@ import torch, synth
 import paper_2108_13191_b200 as g
 shapes = [tuple(int(x) for x in t.split("x")) for t in os.environ.get("SHAPES", "256x256x256,512x512x512,1024x1024x1024,2048x2048x2048,4096x1024x1024,2048x2048x512").split(",")]
 CFGS = [int(c) for c in os.environ.get("CFGS", "1,2,4,5,6").split(",")]
+OPTS = json.loads(os.environ.get("OPTS", "{}"))   # extra gemm_f16 keyword arguments
 R = 20
 for (M, N, K) in shapes:
     for mode in ("f32", "f16"):
@@ -16,11 +17,11 @@ for (M, N, K) in shapes:
         for cfg in CFGS:
             s = torch.cuda.Stream()
             with torch.cuda.stream(s):
-                for _ in range(3): g.gemm_f16(A, B, C, config=cfg)
+                for _ in range(3): g.gemm_f16(A, B, C, config=cfg, **OPTS)
             torch.cuda.synchronize()
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=s):
-                for _ in range(R): g.gemm_f16(A, B, C, config=cfg)
+                for _ in range(R): g.gemm_f16(A, B, C, config=cfg, **OPTS)
             graph.replay(); torch.cuda.synchronize()
             ts = []
             for _ in range(5):
