@@ -306,25 +306,30 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 //    8192 x 1000 x 1000; it loses at 2048^3 and 32768 x 1024 x 4096 on wave quantization).
 int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
   const int64_t pair_tiles = cdiv(M, 256) * cdiv(N, 256);
-  if (M <= 128 || 3 * pair_tiles <= sm_count / 2) {
-    // small output: split K over a cluster when K is long enough to pay for the
-    // DSMEM reduction (profiles/r01/splitk.md; it loses at K <= 2048 with 1024^2)
-    // Each CTA keeps one truncating TMEM chain over its K / S (no promotion, R4):
-    // for F32 C that chain stays <= 4096 long (rel. error <~ 5e-6, bar 1e-5).
+  const bool small = M <= 128 || 3 * pair_tiles <= sm_count / 2;   // under 1/3 wave of pair tiles
+  const bool half = 2 * pair_tiles <= sm_count / 2;                 // at most half a wave
+  if (small || half) {
+    // Few output tiles: split K over a cluster when K is long enough to pay for the
+    // reduction (profiles/r01/splitk.md; it loses at 1024^3).  Each CTA keeps one
+    // truncating TMEM chain over its K / S (no promotion, R4): for F32 C that
+    // chain stays <= 4096 long (rel. error <~ 5e-6, bar 1e-5).
     const int64_t kmax_chain = acc_type == GEMM_ACC_F32 ? 4096 : (int64_t(1) << 40);   // (F16: no limit)
     const int64_t t128 = cdiv(M, 128) * cdiv(N, 128), t256 = cdiv(M, 128) * cdiv(N, 256);
     if (K >= 2048 && 4 * t128 <= sm_count && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x128_S4;
-    // (F32 reduces by TMA reduce-add and prefers S4 from K = 4096; F16 pushes through DSMEM,
-    //  where S2 wins at 1024^2 x 4096 and S4 at 1024^2 x 8192 -- splitk.md)
+    // F32 reduces by TMA reduce-add and prefers S4 from K = 4096 and S2 from K = 2048;
+    // F16 exchanges through DSMEM: S2 from K = 4096, S4 from K = 8192 (splitk.md)
     const int64_t k_s4 = acc_type == GEMM_ACC_F32 ? 4096 : 8192;
+    const int64_t k_s2 = acc_type == GEMM_ACC_F32 ? 2048 : 4096;
     if (K >= k_s4 && 4 * t256 <= sm_count && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S4;
-    if (K >= 4096 && 2 * t256 <= sm_count && K <= 2 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S2;
-    if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
-    return GEMM_CFG_SOLO_128x64;
+    if (K >= k_s2 && 2 * t256 <= sm_count && K <= 2 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S2;
+    if (small) {
+      if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
+      return GEMM_CFG_SOLO_128x64;
+    }
+    // at most half a wave of pair tiles: 128 x 128 tiles keep twice as many SMs busy
+    // (2048 x 1024 x 1024: 9.2-10.5 us vs 12-13 us for the pair tile; profiles/r01/multicast.md)
+    if (t128 <= sm_count) return GEMM_CFG_SOLO_128x128;
   }
-  // at most half a wave of pair tiles: 128 x 128 tiles keep twice as many SMs busy
-  // (2048 x 1024 x 1024: 9.2-10.5 us vs 12-13 us for the pair tile; profiles/r01/multicast.md)
-  if (2 * pair_tiles <= sm_count / 2 && cdiv(M, 128) * cdiv(N, 128) <= sm_count) return GEMM_CFG_SOLO_128x128;
   // F32 C with one K chunk: with the reduce-add epilogue (N % 4 == 0) C_in needs no
   // staging slot, and the 6-stage 64-deep ring is best (profiles/r01/f32_short_k_cfg.txt);
   // a ragged N still stages C_in and keeps the second slot of S5

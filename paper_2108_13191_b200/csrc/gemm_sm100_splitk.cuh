@@ -12,8 +12,8 @@
 // through distributed shared memory, with no workspace and no atomics:
 //   1. cluster barrier: every CTA's mainloop is done, so the operand rings are idle;
 //   2. CTA r owns columns [r BN / S, (r+1) BN / S) of the tile.  Every CTA reads its
-//      partial out of TMEM.  Where everything fits in the idle ring (SKCfg::DMA,
-//      S4 x 128x128) it stages the partial slot-major and sends each owner its slot
+//      partial out of TMEM.  Where everything fits in shared memory (SKCfg::DMA:
+//      S4 x 128x128, and S2 x 128x256 with F16 C) it stages the partial slot-major and sends each owner its slot
 //      with one bulk DMA copy (cp.async.bulk.shared::cluster, counted on the owner's
 //      mbarrier).  Otherwise it pushes each owner's columns into slot r of that
 //      owner's receive buffer with plain 16-byte st.shared::cluster stores
@@ -64,11 +64,12 @@ struct SKCfg {
   // DSMEM exchange by bulk DMA where the own partial (S slots), the S-1 received slots
   // and the C_in slice all fit in the idle ring (S4 x 128x128): one
   // cp.async.bulk.shared::cluster copy per peer instead of 16-byte remote stores
-  static constexpr bool DMA = (2 * S - 1) * SLOT_BYTES + CIN_BYTES <= RING_BYTES;
+  static constexpr int NBAR = 2 * STAGES + 3;            // full[S], empty[S], acc_full, cin, recv
+  static constexpr int POST_DMA = (2 * S - 1) * SLOT_BYTES + CIN_BYTES;
+  static constexpr bool DMA = POST_DMA + 1024 + NBAR * 8 + 16 <= 232448;   // (may extend past the ring)
   static constexpr int OFF_RECV_DMA = S * SLOT_BYTES;
   static constexpr int OFF_CIN_DMA = (2 * S - 1) * SLOT_BYTES;
-  static constexpr int OFF_BAR = RING_BYTES;
-  static constexpr int NBAR = 2 * STAGES + 3;            // full[S], empty[S], acc_full, cin, recv
+  static constexpr int OFF_BAR = (DMA && POST_DMA > RING_BYTES) ? POST_DMA : RING_BYTES;
   static constexpr int SMEM_BYTES = 1024 + OFF_BAR + NBAR * 8 + 16;
   static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of dynamic shared memory");
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
