@@ -219,6 +219,10 @@ gemm_status_t gemm_f16_host(int64_t M, int64_t N, int64_t K,
 /* Configuration gemm_f16 would use for this shape (a gemm_config_t), or -1. */
 int gemm_f16_pick_config(int64_t M, int64_t N, int64_t K, int acc_type);
 
+/* The same table for a given SM count, without touching a device (pure host
+ * function; -1 for a bad mode or sm_count < 2). */
+int gemm_f16_pick_config_for(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count);
+
 /* Static description of a configuration: tile rows/cols, cta_group, pipeline
  * stages, dynamic shared memory bytes.  Returns GEMM_ERR_INVALID_VALUE for an
  * unknown config.  Pure host function (no device needed). */

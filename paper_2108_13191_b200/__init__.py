@@ -43,6 +43,7 @@ _STATUS = {0: "GEMM_OK", 1: "GEMM_ERR_INVALID_VALUE", 2: "GEMM_ERR_MISALIGNED",
            3: "GEMM_ERR_UNSUPPORTED_DEVICE", 4: "GEMM_ERR_CUDA"}
 
 EXPORTED_SYMBOLS = ("gemm_f16", "gemm_f16_ex", "gemm_f16_gather", "gemm_f16_host", "gemm_f16_pick_config",
+                    "gemm_f16_pick_config_for",
                     "gemm_f16_config_info", "gemm_f16_last_launches", "gemm_status_string",
                     "gemm_last_cuda_error")
 
@@ -100,6 +101,8 @@ def load_library(build_if_missing: bool = True):
     lib.gemm_f16_host.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, ci, vp, i64, vp, i64, vp, i64, vp]
     lib.gemm_f16_pick_config.restype = ci
     lib.gemm_f16_pick_config.argtypes = [i64, i64, i64, ci]
+    lib.gemm_f16_pick_config_for.restype = ci
+    lib.gemm_f16_pick_config_for.argtypes = [i64, i64, i64, ci, ci]
     lib.gemm_f16_config_info.restype = ci
     lib.gemm_f16_config_info.argtypes = [ci, ci] + [ctypes.POINTER(ci)] * 5
     lib.gemm_f16_last_launches.restype = ci
@@ -274,8 +277,13 @@ def gemm_f16_host(hA, hB, hC, dA, dB, dC, stream=None):
     return hC
 
 
-def pick_config(M: int, N: int, K: int, acc: int = ACC_F32) -> int:
-    return int(load_library().gemm_f16_pick_config(M, N, K, acc))
+def pick_config(M: int, N: int, K: int, acc: int = ACC_F32, sm_count: int = 0) -> int:
+    """Configuration gemm_f16 would use; with sm_count > 0, the table for that SM count
+    evaluated on the host only (no device needed)."""
+    lib = load_library()
+    if sm_count > 0:
+        return int(lib.gemm_f16_pick_config_for(M, N, K, acc, sm_count))
+    return int(lib.gemm_f16_pick_config(M, N, K, acc))
 
 
 def config_info(config, acc: int = ACC_F32) -> dict:

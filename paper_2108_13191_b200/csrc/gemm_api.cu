@@ -656,6 +656,12 @@ gemm_status_t gemm_f16_host(int64_t M, int64_t N, int64_t K, const void* hA, int
   return GEMM_OK;
 }
 
+int gemm_f16_pick_config_for(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
+  if (acc_type != GEMM_ACC_F32 && acc_type != GEMM_ACC_F16) return -1;
+  if (sm_count < 2 || M < 0 || N < 0 || K < 0) return -1;
+  return pick_config(M, N, K, acc_type, sm_count);
+}
+
 int gemm_f16_pick_config(int64_t M, int64_t N, int64_t K, int acc_type) {
   if (acc_type != GEMM_ACC_F32 && acc_type != GEMM_ACC_F16) return -1;
   int dev = 0;

@@ -1,0 +1,64 @@
+"""The shape -> kernel-configuration table (gemm_api.cu pick_config; the paper's per-size
+"best performing version"), evaluated on the host for the B200's 148 SMs.
+
+Every expectation below is a measured winner (profiles/r01: cfgsweep.md, wide_tile.md,
+f32_short_k_cfg.txt, multicast.md, splitk.md v8/v9, mid_size_configs.txt).  The F32 chain
+limit of the split-K configs (R4/R17) is checked as an invariant over a grid."""
+import itertools
+
+import pytest
+
+import paper_2108_13191_b200 as g
+
+SM = 148
+C = g.CONFIGS
+
+CASES = [
+    # (M, N, K, acc, expected config name)
+    (8192, 8192, 8192, 0, "pair_256x256_k128"),      # bench F32
+    (8192, 8192, 8192, 1, "pair_256x512"),           # bench F16: the wide tile
+    (16384, 16384, 16384, 1, "pair_256x512"),
+    (4096, 4096, 4096, 1, "pair_256x512"),
+    (2048, 2048, 2048, 1, "pair_256x256_k128"),      # wide fills the last wave worse
+    (32768, 1024, 4096, 1, "pair_256x256_k128"),
+    (16384, 4096, 1024, 0, "pair_256x256"),          # F32 one K chunk, reduce-add epilogue
+    (8192, 1002, 1000, 0, "pair_256x256_s5"),        # ... but a ragged N (N % 4 != 0) still stages C_in
+    (1024, 1024, 1024, 0, "solo_128x64"),            # BASELINE configs[1]-sized
+    (1024, 1024, 1024, 1, "solo_128x64"),
+    (2048, 1024, 1024, 0, "solo_128x128"),           # at most half a wave of pair tiles
+    (256, 1024, 16384, 1, "splitk_128x128_s4"),      # small output, long K
+    (512, 512, 8192, 0, "splitk_128x128_s4"),
+    (1024, 1024, 4096, 0, "splitk_128x256_s4"),      # F32 prefers S4 from K = 4096
+    (1024, 1024, 4096, 1, "splitk_128x256_s2"),      # F16 prefers S2 there
+    (1024, 1024, 8192, 1, "splitk_128x256_s4"),
+    (1024, 2048, 4096, 0, "splitk_128x256_s2"),
+    (1024, 1024, 2048, 0, "splitk_128x256_s2"),      # F32 S2 from K = 2048
+    (1024, 1024, 2048, 1, "solo_128x64"),            # F16 not yet
+]
+
+
+@pytest.mark.parametrize("M,N,K,acc,want", CASES)
+def test_measured_winners(M, N, K, acc, want):
+    assert g.pick_config(M, N, K, acc, sm_count=SM) == C[want], (M, N, K, acc)
+
+
+def test_f32_split_chain_never_exceeds_4096():
+    # each split CTA keeps one truncating TMEM chain over K / S: for F32 C it must stay
+    # <= 4096 long (rel. error ~5e-6 against the 1e-5 bar); F16 has no such limit
+    splits = {C["splitk_128x256_s2"]: 2, C["splitk_128x256_s4"]: 4, C["splitk_128x128_s4"]: 4}
+    seen = set()
+    for M, N, K in itertools.product([64, 128, 256, 512, 1024, 2048], [64, 256, 512, 1024, 2048, 4096],
+                                     [1024, 2048, 4096, 8192, 16384, 32768, 65536]):
+        for acc in (0, 1):
+            cfg = g.pick_config(M, N, K, acc, sm_count=SM)
+            assert cfg > 0
+            if cfg in splits:
+                seen.add((acc, cfg))
+                if acc == 0:
+                    assert -(-K // splits[cfg]) <= 4096, (M, N, K, cfg)
+    assert {(0, C["splitk_128x128_s4"]), (1, C["splitk_128x128_s4"])} <= seen
+
+
+def test_bad_arguments():
+    assert g.pick_config(8, 8, 8, 7, sm_count=SM) == -1
+    assert g.pick_config(8, 8, 8, 0, sm_count=1) == -1
