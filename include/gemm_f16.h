@@ -85,7 +85,8 @@ typedef enum {
   GEMM_CFG_SOLO_128x64_MC4 = 13,  /* as SOLO_128x64 in 4-CTA clusters along N: each CTA loads a quarter
                                      of the shared A box and TMA-multicasts it to the other three */
   GEMM_CFG_SOLO_128x128_MC4 = 14, /* as SOLO_128x128, with the same A multicast */
-  GEMM_CFG_COUNT = 15
+  GEMM_CFG_SPLITK_128x128_S2 = 15, /* as SPLITK_128x128_S4 with 2 CTAs (halves of K) per cluster */
+  GEMM_CFG_COUNT = 16
 } gemm_config_t;
 
 typedef struct {

@@ -38,6 +38,7 @@ CONFIGS = {
     "splitk_128x128_s4": 12,
     "solo_128x64_mc4": 13,
     "solo_128x128_mc4": 14,
+    "splitk_128x128_s2": 15,
 }
 _STATUS = {0: "GEMM_OK", 1: "GEMM_ERR_INVALID_VALUE", 2: "GEMM_ERR_MISALIGNED",
            3: "GEMM_ERR_UNSUPPORTED_DEVICE", 4: "GEMM_ERR_CUDA"}

@@ -108,6 +108,7 @@ const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
     make_splitk_desc<128, 4>(),
     make_desc<Cfg13F32, Cfg13F16>(),
     make_desc<Cfg14F32, Cfg14F16>(),
+    make_splitk_desc<128, 2>(),
 };
 using CfgW16 = WCfg<4>;
 const ConfigDesc kWideConfig{2, CfgW16::BN, CfgW16::STAGES, CfgW16::THREADS, CfgW16::BK,
@@ -315,13 +316,18 @@ int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
     // chain stays <= 4096 long (rel. error <~ 5e-6, bar 1e-5).
     const int64_t kmax_chain = acc_type == GEMM_ACC_F32 ? 4096 : (int64_t(1) << 40);   // (F16: no limit)
     const int64_t t128 = cdiv(M, 128) * cdiv(N, 128), t256 = cdiv(M, 128) * cdiv(N, 256);
-    if (K >= 2048 && 4 * t128 <= sm_count && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x128_S4;
-    // F32 reduces by TMA reduce-add and prefers S4 from K = 4096 and S2 from K = 2048;
-    // F16 exchanges through DSMEM: S2 from K = 4096, S4 from K = 8192 (splitk.md)
-    const int64_t k_s4 = acc_type == GEMM_ACC_F32 ? 4096 : 8192;
-    const int64_t k_s2 = acc_type == GEMM_ACC_F32 ? 2048 : 4096;
-    if (K >= k_s4 && 4 * t256 <= sm_count && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S4;
-    if (K >= k_s2 && 2 * t256 <= sm_count && K <= 2 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S2;
+    // 4-CTA clusters: only ~132 of 148 SMs can hold them at once (tools/probe_cluster.cu)
+    const int64_t sm4 = sm_count - sm_count / 9;
+    const bool f32 = acc_type == GEMM_ACC_F32;
+    if (K >= 2048 && 4 * t128 <= sm4 && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x128_S4;
+    // F32 reduces by TMA reduce-add: S4 x 128x256 from K = 4096, S2 x 128x128 from K = 1024,
+    // S2 x 128x256 from K = 2048.  F16 exchanges through DSMEM, where the bulk-DMA configs
+    // (S2 x 128x128, S2 x 128x256) beat the pushes of S4 x 128x256 until K = 16384
+    // (splitk.md v9/v10)
+    if (f32 && K >= 4096 && 4 * t256 <= sm4 && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S4;
+    if (!f32 && K >= 16384 && 4 * t256 <= sm4) return GEMM_CFG_SPLITK_128x256_S4;
+    if (K >= (f32 ? 1024 : 2048) && 2 * t128 <= sm_count && K <= 2 * kmax_chain) return GEMM_CFG_SPLITK_128x128_S2;
+    if (K >= (f32 ? 2048 : 4096) && 2 * t256 <= sm_count && K <= 2 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S2;
     if (small) {
       if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
       return GEMM_CFG_SOLO_128x64;

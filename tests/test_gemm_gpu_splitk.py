@@ -19,7 +19,7 @@ from parity import Guarded, check, device_problem, oracle_full, round_up
 
 pytestmark = pytest.mark.gpu
 
-SPLIT = ["splitk_128x256_s2", "splitk_128x256_s4", "splitk_128x128_s4"]
+SPLIT = ["splitk_128x256_s2", "splitk_128x256_s4", "splitk_128x128_s4", "splitk_128x128_s2"]
 
 
 @pytest.fixture(scope="module")
@@ -156,8 +156,8 @@ def test_splitk_auto_long_k_accuracy(g, shape):
     # chain <= 4096 long (R4), so the error stays well under the 1e-5 bar
     import torch
     M, N, K = shape
-    assert g.pick_config(M, N, K, g.ACC_F32) in (10, 11, 12)
-    assert g.pick_config(M, N, K, g.ACC_F16) in (10, 11, 12)
+    assert g.pick_config(M, N, K, g.ACC_F32) in (10, 11, 12, 15)
+    assert g.pick_config(M, N, K, g.ACC_F16) in (10, 11, 12, 15)
     for acc in ("f32", "f16"):
         A, B, C = synth.problem(M, N, K, acc, seed=11)
         dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))

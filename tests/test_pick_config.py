@@ -23,17 +23,22 @@ CASES = [
     (32768, 1024, 4096, 1, "pair_256x256_k128"),
     (16384, 4096, 1024, 0, "pair_256x256"),          # F32 one K chunk, reduce-add epilogue
     (8192, 1002, 1000, 0, "pair_256x256_s5"),        # ... but a ragged N (N % 4 != 0) still stages C_in
-    (1024, 1024, 1024, 0, "solo_128x64"),            # BASELINE configs[1]-sized
+    (1024, 1024, 1024, 0, "splitk_128x128_s2"),      # F32: split in two even at K = 1024
     (1024, 1024, 1024, 1, "solo_128x64"),
     (2048, 1024, 1024, 0, "solo_128x128"),           # at most half a wave of pair tiles
     (256, 1024, 16384, 1, "splitk_128x128_s4"),      # small output, long K
     (512, 512, 8192, 0, "splitk_128x128_s4"),
     (1024, 1024, 4096, 0, "splitk_128x256_s4"),      # F32 prefers S4 from K = 4096
-    (1024, 1024, 4096, 1, "splitk_128x256_s2"),      # F16 prefers S2 there
-    (1024, 1024, 8192, 1, "splitk_128x256_s4"),
+    (1024, 1024, 4096, 1, "splitk_128x128_s2"),      # F16: the bulk-DMA S2 configs
+    (1024, 1024, 8192, 1, "splitk_128x128_s2"),
+    (1024, 1024, 16384, 1, "splitk_128x256_s4"),
     (1024, 2048, 4096, 0, "splitk_128x256_s2"),
-    (1024, 1024, 2048, 0, "splitk_128x256_s2"),      # F32 S2 from K = 2048
-    (1024, 1024, 2048, 1, "solo_128x64"),            # F16 not yet
+    (1024, 1024, 2048, 0, "splitk_128x128_s2"),
+    (1024, 1024, 2048, 1, "splitk_128x128_s2"),
+    (1024, 512, 1024, 0, "splitk_128x128_s2"),
+    (768, 768, 2048, 0, "splitk_128x128_s2"),        # 36 x 4 CTAs would not fit in 4-CTA clusters
+    (768, 768, 2048, 1, "splitk_128x128_s2"),
+    (512, 512, 1024, 1, "solo_128x64"),              # F16 S2 only from K = 2048
 ]
 
 
@@ -45,7 +50,8 @@ def test_measured_winners(M, N, K, acc, want):
 def test_f32_split_chain_never_exceeds_4096():
     # each split CTA keeps one truncating TMEM chain over K / S: for F32 C it must stay
     # <= 4096 long (rel. error ~5e-6 against the 1e-5 bar); F16 has no such limit
-    splits = {C["splitk_128x256_s2"]: 2, C["splitk_128x256_s4"]: 4, C["splitk_128x128_s4"]: 4}
+    splits = {C["splitk_128x256_s2"]: 2, C["splitk_128x256_s4"]: 4, C["splitk_128x128_s4"]: 4,
+              C["splitk_128x128_s2"]: 2}
     seen = set()
     for M, N, K in itertools.product([64, 128, 256, 512, 1024, 2048], [64, 256, 512, 1024, 2048, 4096],
                                      [1024, 2048, 4096, 8192, 16384, 32768, 65536]):
