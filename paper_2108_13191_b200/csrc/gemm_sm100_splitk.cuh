@@ -65,11 +65,13 @@ struct SKCfg {
   // and the C_in slice all fit in the idle ring (S4 x 128x128): one
   // cp.async.bulk.shared::cluster copy per peer instead of 16-byte remote stores
   static constexpr int NBAR = 2 * STAGES + 3;            // full[S], empty[S], acc_full, cin, recv
-  static constexpr int POST_DMA = (2 * S - 1) * SLOT_BYTES + CIN_BYTES;
-  static constexpr bool DMA = POST_DMA + 1024 + NBAR * 8 + 16 <= 232448;   // (may extend past the ring)
+  // the C_in slice lives past both the ring and the exchange buffers, so its TMA load
+  // can be issued at kernel start and land under the mainloop
+  static constexpr int OFF_CIN_DMA = RING_BYTES > (2 * S - 1) * SLOT_BYTES ? RING_BYTES : (2 * S - 1) * SLOT_BYTES;
+  static constexpr int POST_DMA = OFF_CIN_DMA + CIN_BYTES;
+  static constexpr bool DMA = POST_DMA + 1024 + NBAR * 8 + 16 <= 232448;
   static constexpr int OFF_RECV_DMA = S * SLOT_BYTES;
-  static constexpr int OFF_CIN_DMA = (2 * S - 1) * SLOT_BYTES;
-  static constexpr int OFF_BAR = (DMA && POST_DMA > RING_BYTES) ? POST_DMA : RING_BYTES;
+  static constexpr int OFF_BAR = DMA ? POST_DMA : RING_BYTES;
   static constexpr int SMEM_BYTES = 1024 + OFF_BAR + NBAR * 8 + 16;
   static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of dynamic shared memory");
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
@@ -150,6 +152,13 @@ gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
     // ===================== TMA producer: this CTA's share of K =====================
     if (lane == 0) {
       griddep_launch_dependents();
+      if constexpr (Cfg::DMA) {
+        if (load_c) {   // C_in slice now (its own region), ready long before the reduction
+          mbar_arrive_expect_tx(cin_bar, Cfg::CIN_BYTES);
+          tma_load_2d_hint(base + Cfg::OFF_CIN_DMA, &tm_cin, tn * BN + static_cast<int>(r) * CW, tm * BM, cin_bar,
+                           policy_evict_first());
+        }
+      }
       const uint64_t pol = policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
@@ -248,10 +257,6 @@ gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
     const uint32_t sStage = base;                         // own partial, slot-major by owner
     const uint32_t sRecv = base + Cfg::OFF_RECV_DMA;      // S-1 slots from the peers
     const uint32_t sCin = base + Cfg::OFF_CIN_DMA;        // this CTA's C_in slice
-    if (warp == Cfg::W_PRODUCER && lane == 0 && load_c) {
-      mbar_arrive_expect_tx(cin_bar, Cfg::CIN_BYTES);
-      tma_load_2d_hint(sCin, &tm_cin, tn * BN + static_cast<int>(r) * CW, tm * BM, cin_bar, policy_evict_first());
-    }
     if (warp < 4) {
       const uint32_t row = warp * 32 + lane;
       const uint32_t t_row = tmem_base + ((warp * 32u) << 16);
