@@ -351,6 +351,7 @@ gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
         }
       }
     }
+    if (tr) p.trace[7] = globaltimer_ns();
     // every copy into every CTA has landed (each owner waited) before any CTA exits:
     // the copies read their senders' shared memory
     __syncwarp();

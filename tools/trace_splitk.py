@@ -14,6 +14,6 @@ for spec in sys.argv[1:]:
     for _ in range(3): g.gemm_f16(A, B, C, config=cfg)
     g.gemm_f16(A, B, C, config=cfg, trace=tr, **kw)
     torch.cuda.synchronize()
-    t = tr.cpu().numpy()[:7]
-    names = ["entry", "setup", "acc_ready", "all_mainloops_done", "pushed", "cin_in", "exit"]
+    t = tr.cpu().numpy()[:8]
+    names = ["entry", "setup", "acc_ready", "all_mainloops_done", "pushed", "recv_in", "exit", "reduced"]
     print(spec, " ".join(f"{n}={(x - t[0]) / 1000:.2f}us" for n, x in zip(names, t)))
