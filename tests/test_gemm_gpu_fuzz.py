@@ -2,6 +2,8 @@
 odd sizes), random padded leading dims, random configurations and scheduling /
 epilogue options, both output modes and both input types; guard bands must stay
 untouched.  Every case is reproducible from its index."""
+import os
+
 import numpy as np
 import pytest
 
@@ -33,7 +35,18 @@ def test_fuzz_wide_tile_against_oracle(case):
     _fuzz_case(case, 20_000 + case, wide=True)
 
 
-def _fuzz_case(case, seed, wide):
+SPLIT_AND_MC = ["splitk_128x256_s2", "splitk_128x256_s4", "splitk_128x128_s4", "splitk_128x128_s2",
+                "solo_128x64_mc4", "solo_128x128_mc4"]
+N_EXTRA = int(os.environ.get("FUZZ_EXTRA", "24"))   # a longer campaign: FUZZ_EXTRA=300
+
+
+@pytest.mark.parametrize("case", range(N_EXTRA))
+def test_fuzz_split_and_multicast_against_oracle(case):
+    # the cluster kernels: split-K (DSMEM / bulk-DMA / reduce-add paths) and A multicast
+    _fuzz_case(case, 30_000 + case, wide=False, configs=SPLIT_AND_MC)
+
+
+def _fuzz_case(case, seed, wide, configs=None):
     import torch
     import paper_2108_13191_b200 as g
     rng = np.random.default_rng(seed)
@@ -42,7 +55,7 @@ def _fuzz_case(case, seed, wide):
     K = int(rng.choice([1, 15, 16, 17, 63, 64, 65, 128, 129]) if rng.random() < 0.3 else rng.integers(1, 1500))
     acc = "f32" if rng.random() < 0.5 else "f16"
     bf16 = rng.random() < 0.25
-    kw = {"config": str(rng.choice(CONFIGS))}
+    kw = {"config": str(rng.choice(configs or CONFIGS))}
     if wide:
         acc, kw["config"] = "f16", "pair_256x512"
         N = int(rng.integers(1, 2600))
@@ -58,6 +71,8 @@ def _fuzz_case(case, seed, wide):
         kw["ring_stages"] = int(rng.integers(1, 5))
     if rng.random() < 0.2:
         kw["k_serpentine"] = 1
+    if kw["config"].startswith("splitk") and kw.get("promote_k", 0) > 0:
+        kw["promote_k"] = -1      # split configs keep one chain per K share by design
     beta = 0 if rng.random() < 0.2 else 1
     relu = rng.random() < 0.2
     use_bias = rng.random() < 0.25
