@@ -336,6 +336,12 @@ int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
     // (2048 x 1024 x 1024: 9.2-10.5 us vs 12-13 us for the pair tile; profiles/r01/multicast.md)
     if (t128 <= sm_count) return GEMM_CFG_SOLO_128x128;
   }
+  // one wave of pair tiles or less (each cluster runs at most one tile) with K <= 4096:
+  // nothing follows a tile's epilogue, so its stores are fully exposed and the 3 staging
+  // slots of the 4 x 32 KB ring pipeline them best (2048^3: 18.9 vs 20.1 us F32, 17.9 vs
+  // 18.8 us F16; it loses ~4 % at K = 8192, where the deeper ring matters more;
+  // profiles/r01/single_wave_cfg.txt)
+  if (pair_tiles <= sm_count / 2 && K <= 4096) return GEMM_CFG_PAIR_256x256_S4;
   // F32 C with one K chunk: with the reduce-add epilogue (N % 4 == 0) C_in needs no
   // staging slot, and the 6-stage 64-deep ring is best (profiles/r01/f32_short_k_cfg.txt);
   // a ragged N still stages C_in and keeps the second slot of S5

@@ -19,7 +19,13 @@ CASES = [
     (8192, 8192, 8192, 1, "pair_256x512"),           # bench F16: the wide tile
     (16384, 16384, 16384, 1, "pair_256x512"),
     (4096, 4096, 4096, 1, "pair_256x512"),
-    (2048, 2048, 2048, 1, "pair_256x256_k128"),      # wide fills the last wave worse
+    (2048, 2048, 2048, 1, "pair_256x256_s4"),        # one wave: 3 staging slots pipeline the stores
+    (2048, 2048, 2048, 0, "pair_256x256_s4"),
+    (1536, 3072, 2048, 0, "pair_256x256_s4"),
+    (2048, 2048, 4096, 1, "pair_256x256_s4"),
+    (2048, 2048, 8192, 0, "pair_256x256_k128"),      # ... but not at K = 8192
+    (2560, 2048, 2048, 0, "pair_256x256"),           # 80 pair tiles: more than one wave
+    (3072, 3072, 2048, 1, "pair_256x512"),
     (32768, 1024, 4096, 1, "pair_256x256_k128"),
     (16384, 4096, 1024, 0, "pair_256x256"),          # F32 one K chunk, reduce-add epilogue
     (8192, 1002, 1000, 0, "pair_256x256_s5"),        # ... but a ragged N (N % 4 != 0) still stages C_in
