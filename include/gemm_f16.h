@@ -120,7 +120,9 @@ typedef struct {
   int relu;         /* 1: max(x, 0) applied before rounding (NaN propagates)              */
   const void* bias; /* NULL, or device float[N] added to every row (16-byte aligned)      */
   void* trace;      /* DIAGNOSTIC ONLY, normally NULL: device buffer of 512 uint64 that   */
-                    /* receives per-tile globaltimer stamps of CTA 0                      */
+                    /* receives per-tile globaltimer stamps of CTA 0 (256x256-class pair  */
+                    /* and 1-CTA kernels: of the CTA whose index the caller put in        */
+                    /* element 511 before the call)                                       */
   int accum_f16;    /* EXPERIMENT, 0 normally: 1 = the tensor core accumulates in binary16 */
                     /* (instruction c_format F16: the paper's literal F16 accumulation,   */
                     /* P:979-980; DESIGN R3/R16).  Partial sums are still promoted into   */
@@ -135,6 +137,16 @@ typedef struct {
                     /* adds its tile into C with a TMA reduce-add store instead of loading */
                     /* C_in into shared memory (bitwise the same single RN add); -1 = off; */
                     /* 0 = default (on)                                                     */
+  int stream_k;     /* F32 C on a CTA-pair config, reduce-add epilogue: 1 = when the last    */
+                    /* wave of tiles is partial, share the last partial wave plus one full  */
+                    /* wave out over all clusters as equal runs of k-blocks (split tiles    */
+                    /* meet in C by two reduce-adds in a fixed order; deterministic for a   */
+                    /* given grid); 0 = default (on when max_clusters is 0 and the last     */
+                    /* wave is <= 50 % full with K >= 4096, or <= 30 % full with K > 2048); */
+                    /* -1 = off                                                             */
+  int tail_ring;    /* 0: default (on); -1: off.  On a CTA's last tile, when no C_in is     */
+                    /* staged, all output chunks are staged at once in the idle operand    */
+                    /* ring and stored back to back (256x256-class pair and 1-CTA configs) */
 } gemm_options_t;
 
 /*

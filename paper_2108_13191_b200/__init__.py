@@ -67,7 +67,8 @@ class _Options(ctypes.Structure):
                 ("c_row_prefetch", ctypes.c_int), ("in_type", ctypes.c_int), ("beta0", ctypes.c_int),
                 ("relu", ctypes.c_int), ("bias", ctypes.c_void_p), ("trace", ctypes.c_void_p),
                 ("accum_f16", ctypes.c_int), ("pdl", ctypes.c_int), ("raster", ctypes.c_int),
-                ("c_reduce", ctypes.c_int)]
+                ("c_reduce", ctypes.c_int), ("stream_k", ctypes.c_int),
+                ("tail_ring", ctypes.c_int)]
 
 
 _lib = None
@@ -155,7 +156,8 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
              debug_flags: int = 0, promote_k: int = 0, epi_pace: int = 0, ring_stages: int = 0,
              acc_bufs: int = 0, k_serpentine: int = 0, wait_hint_ns: int = 0, c_row_prefetch: int = 0,
              beta: int = 1, bias=None, relu: bool = False, trace=None, accum_f16: bool = False,
-             pdl: int = 0, raster: int = 0, c_reduce: int = 0):
+             pdl: int = 0, raster: int = 0, c_reduce: int = 0, stream_k: int = 0,
+             tail_ring: int = 0):
     """In place: C += A @ B on the GPU (enqueued on `stream`, default: torch's current).
 
     A: (M, K) torch.float16 or torch.bfloat16 CUDA, B: (K, N) of the same dtype,
@@ -196,7 +198,7 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
         if (cfg == 0 and not max_clusters and not group_m and not l2_hints and not debug_flags and not promote_k
                 and not epi_pace and not ring_stages and not acc_bufs and not k_serpentine and not wait_hint_ns
                 and not c_row_prefetch and trace is None and in_type == 0 and beta == 1 and bias is None
-                and not relu and not accum_f16 and not pdl and not raster and not c_reduce):
+                and not relu and not accum_f16 and not pdl and not raster and not c_reduce and not stream_k and not tail_ring):
             st = lib.gemm_f16(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
                               C.data_ptr(), _ld(C, "C"), acc, sh)
         else:
@@ -205,7 +207,7 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
                             int(wait_hint_ns), int(c_row_prefetch), in_type, 1 - int(beta), int(bool(relu)),
                             None if bias is None else ctypes.c_void_p(bias.data_ptr()),
                             None if trace is None else ctypes.c_void_p(trace.data_ptr()), int(bool(accum_f16)),
-                            int(pdl), int(raster), int(c_reduce))
+                            int(pdl), int(raster), int(c_reduce), int(stream_k), int(tail_ring))
             st = lib.gemm_f16_ex(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
                                  C.data_ptr(), _ld(C, "C"), acc, sh, ctypes.byref(opts))
     finally:

@@ -31,6 +31,15 @@ constexpr int kDefaultCRowPrefetch = 0;
 constexpr int kDefaultPdl = 1;   // profiles/r01/findings.md section 9
 constexpr int kDefaultSnake = 0;
 constexpr int kDefaultCReduce = 1;   // findings.md section 14: +1-10 %, bitwise identical
+// stream-K (auto): taken when the last wave of tiles is at most this full, K >= 4096 ...
+constexpr double kStreamKMaxFill = 0.5;
+// ... or at most this full with K > 2048 (profiles/r01/stream_k.md: the K = 1024-2048 tiles
+// are too short to pay for the extra partial-tile store phases)
+constexpr double kStreamKMaxFillShortK = 0.3;
+
+// token counters of the stream-K hand-over (gemm_sm100.cuh): every launch leaves them at
+// zero (each posted token is taken), so no per-launch reset and no allocation is needed
+__device__ unsigned g_sk_flags[kSkFlagSlots];
 
 thread_local int t_last_cuda_error = 0;
 thread_local int t_last_launches = 0;
@@ -73,14 +82,22 @@ struct ConfigDesc {
   int k_splits = 0;   // split-K configs: CTAs per cluster sharing one tile's K (non-persistent grid)
   int a_mc = 1;       // A-multicast configs: CTAs per cluster sharing A (tiles (tm, a_mc * tg + r))
   int cluster_size() const { return cluster ? cluster : cta_group; }
+  KernelFn sk_fn = nullptr;   // F32 C, stream-K build (CTA-pair tiles only)
 };
+
+template <class C>
+constexpr KernelFn sk_fn_of() {
+  if constexpr (C::CG == 2 && !C::PEERS && C::MC == 1 && !C::OUT_F16) return &gemm_f16_sm100_kernel<C, true>;
+  else return nullptr;
+}
 
 template <class C32, class C16>
 constexpr ConfigDesc make_desc() {
   return ConfigDesc{C32::CG, C32::BN, C32::STAGES, C32::THREADS, C32::BK,
                     {C32::SMEM_BYTES, C16::SMEM_BYTES}, {C32::CW, C16::CW}, {C32::RB, C16::RB},
                     {&gemm_f16_sm100_kernel<C32>, &gemm_f16_sm100_kernel<C16>},
-                    C32::MC > 1 ? C32::MC : 0, 0, C32::MC};
+                    C32::MC > 1 ? C32::MC : 0, 0, C32::MC,
+                    sk_fn_of<C32>()};
 }
 
 template <int BN, int S>
@@ -135,6 +152,7 @@ struct DeviceInfo {
   int cuda_error = 0;
   int sm_count = 0;
   int max_clusters[GEMM_CFG_COUNT + 1][2] = {};   // [GEMM_CFG_COUNT] = the gather config
+  unsigned* sk_flags = nullptr;                    // this device's g_sk_flags
 };
 std::once_flag g_dev_once[kMaxDevices];
 DeviceInfo g_dev[kMaxDevices];
@@ -173,6 +191,11 @@ void init_device(int dev) {
         e = cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(cd.fn[a]), &lc);
         if (e != cudaSuccess || n <= 0) { d.status = GEMM_ERR_CUDA; d.cuda_error = e ? e : cudaErrorInvalidConfiguration; return; }
         d.max_clusters[c][a] = n;
+        if (a == GEMM_ACC_F32 && cd.sk_fn != nullptr) {   // the stream-K build: same smem, same cluster
+          e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.sk_fn),
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, cd.smem[a]);
+          if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
+        }
         if (c == GEMM_CFG_PAIR_256x512) {   // the option-carrying twin: same smem, same cluster
           e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kWideExtFn),
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, cd.smem[a]);
@@ -186,6 +209,10 @@ void init_device(int dev) {
       }
     }
   }
+  void* f = nullptr;
+  e = cudaGetSymbolAddress(&f, g_sk_flags);
+  if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
+  d.sk_flags = static_cast<unsigned*>(f);
 }
 
 // Copy streams of the host-buffer path (created once per device, never destroyed).
@@ -545,6 +572,29 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   }
   lc.attrs = lc.numAttrs ? attr : nullptr;
   KernelFn fn = cd.fn[a];
+  // stream-K: when the last wave of tiles is partial, the last partial wave plus one full
+  // wave are shared out over all clusters as equal runs of k-blocks (gemm_sm100.cuh Work);
+  // the partial tiles meet in C through the reduce-add epilogue, in a fixed order
+  const int tro = opts ? opts->tail_ring : 0;
+  if (tro < -1 || tro > 1) return GEMM_ERR_INVALID_VALUE;
+  p.tail_ring = tro >= 0 ? 1 : 0;
+  const int skopt = opts ? opts->stream_k : 0;
+  if (skopt < -1 || skopt > 1) return GEMM_ERR_INVALID_VALUE;
+  p.sk_tile0 = p.num_tiles;
+  const bool sk_ok = cd.sk_fn != nullptr && a == GEMM_ACC_F32 && n_peers == 0 && p.c_reduce && !p.beta0 &&
+                     p.bias == nullptr && !p.relu && !p.c_ragged && p.debug_flags == 0 && !p.k_serpentine &&
+                     p.c_row_prefetch != 2 && clusters * 16 <= kSkFlagSlots &&
+                     (tiles % clusters + clusters) * static_cast<int64_t>(p.k_blocks) < 0x7fffffffLL;
+  const int64_t rem = tiles % clusters, waves = tiles / clusters;
+  const double fill = static_cast<double>(rem) / clusters;
+  const bool sk_want = skopt > 0 || (skopt == 0 && !(opts && opts->max_clusters > 0) &&
+                                      ((K >= 4096 && fill <= kStreamKMaxFill) ||
+                                       (K > 2048 && fill <= kStreamKMaxFillShortK)));
+  if (sk_ok && sk_want && waves >= 1 && rem > 0) {
+    p.sk_tile0 = static_cast<int>(tiles - rem - clusters);
+    p.sk_flags = di.sk_flags;
+    fn = cd.sk_fn;
+  }
   if (cfg == GEMM_CFG_PAIR_256x512 && (p.bias != nullptr || p.relu || p.accum_f16)) fn = kWideExtFn;
   cudaError_t e = cudaLaunchKernelEx(&lc, fn, tm_a, tm_b, tm_c, p, pm, tm_cpf);
   if (e != cudaSuccess) return cuda_fail(e);

@@ -91,7 +91,76 @@ struct GemmParams {
   int l2_hints;                     // 1: TMA loads/stores carry L2 eviction-priority hints
                                     // (A evict_last: re-read by the next wave of tiles;
                                     //  C evict_first: streamed once)
+  // stream-K (kernel built with SK = true; F32 C with the reduce-add epilogue only):
+  // tiles [sk_tile0, num_tiles) are shared out as equal runs of (tile, k-block) units, one
+  // run per cluster, so the last partial wave is spread over every cluster
+  int sk_tile0;
+  unsigned* sk_flags;               // token counters, one per (cluster boundary, CTA, epilogue warp)
+  int tail_ring;                    // 1: the last tile's output chunks are staged all at once in the
+                                    // (then idle) operand ring instead of cycling through the slots
 };
+
+// The work of one cluster, in the order it is processed: its data-parallel tiles
+// cluster, cluster + ncl, ... below sk_tile0, then its run [u0, u1) of the stream-K units
+// (unit = tile * k_blocks + k-block over the stream-K tiles), tile by tile from the LAST
+// tile of the run down.  A tile split between clusters c and c + 1 is therefore the first
+// item of c (k-blocks [0, x)) and the last item of c + 1 (k-blocks [x, k_blocks)): c adds
+// its partial into C first and posts a token; c + 1 takes it before adding its own, so the
+// two reduce-adds into C happen in a fixed order (deterministic result), and a cluster
+// only ever waits on a lower-numbered one that did that work first.  The host gives every
+// cluster at least k_blocks units, so a tile is split at most once.
+struct Work {
+  int n_dp, n_items, t_hi;
+  int u0, u1;   // (the host keeps the stream-K unit count below 2^31)
+};
+struct Item {
+  int tile, kb_lo, kb_hi;
+  bool wait, signal;   // wait: k-blocks [0, kb_lo) are cluster-1's; signal: [kb_hi, k_blocks) are cluster+1's
+};
+// token counter of (cluster boundary b, CTA rank, epilogue warp): the writer warp and
+// the waiting warp cover the same 32 x BN/2 region of the shared tile
+constexpr int kSkFlagSlots = 4096;
+__device__ __forceinline__ int sk_slot(int b, uint32_t rank, uint32_t ew) {
+  return (b * 2 + static_cast<int>(rank)) * 8 + static_cast<int>(ew);
+}
+template <bool SK>
+__device__ __forceinline__ Work work_of(const GemmParams& p, int cluster, int ncl) {
+  Work w;
+  const int dp_end = SK ? p.sk_tile0 : p.num_tiles;
+  w.n_dp = cluster < dp_end ? (dp_end - cluster + ncl - 1) / ncl : 0;
+  w.n_items = w.n_dp;
+  w.t_hi = 0;
+  w.u0 = w.u1 = 0;
+  if constexpr (SK) {
+    const long long units = static_cast<long long>(p.num_tiles - p.sk_tile0) * p.k_blocks;
+    w.u0 = static_cast<int>(units * cluster / ncl);
+    w.u1 = static_cast<int>(units * (cluster + 1) / ncl);
+    if (w.u1 > w.u0) {
+      w.t_hi = (w.u1 - 1) / p.k_blocks;
+      w.n_items += w.t_hi - w.u0 / p.k_blocks + 1;
+    }
+  }
+  return w;
+}
+template <bool SK>
+__device__ __forceinline__ Item item_of(const GemmParams& p, const Work& w, int cluster, int ncl, int i) {
+  Item it;
+  if (!SK || i < w.n_dp) {
+    it.tile = cluster + i * ncl;
+    it.kb_lo = 0;
+    it.kb_hi = p.k_blocks;
+    it.wait = it.signal = false;
+    return it;
+  }
+  const int t = w.t_hi - (i - w.n_dp);
+  const int t0 = t * p.k_blocks;
+  it.tile = p.sk_tile0 + t;
+  it.kb_lo = max(w.u0, t0) - t0;
+  it.kb_hi = min(w.u1, t0 + p.k_blocks) - t0;
+  it.wait = it.kb_lo > 0;
+  it.signal = it.kb_hi < p.k_blocks;
+  return it;
+}
 
 template <int CG_, int BN_, int STAGES_, bool OUT_F16_, int EPI_SLOTS_ = 1, int BK_ = 64, bool PEERS_ = false,
           int MC_ = 1>
@@ -129,6 +198,8 @@ struct KCfg {
   static constexpr int EPI_SLOTS = EPI_SLOTS_;
   static constexpr int PRE = (EPI_SLOTS < NOUT) ? EPI_SLOTS : NOUT;   // C_in chunks loaded at tile start
   static constexpr int EPI_BUF = 32 * 128;            // 32 rows x up to 128 B
+  // the last tile of a CTA can stage every output chunk at once in the idle operand ring
+  static constexpr bool TAIL_RING = NOUT > EPI_SLOTS && EPI_WARPS * NOUT * EPI_BUF <= STAGES * (A_BYTES + B_BYTES);
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = STAGES * A_BYTES;
   static constexpr int OFF_E = STAGES * STAGE_BYTES;
@@ -196,7 +267,7 @@ __device__ __forceinline__ float4 load_bias4(const float* bias, int col, int n) 
 }
 __device__ __forceinline__ float relu_keep_nan(float x) { return (x > 0.f || x != x) ? x : 0.f; }
 
-template <class Cfg>
+template <class Cfg, bool SK = false>
 __global__ void __launch_bounds__(352, 1)
 gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                       const __grid_constant__ CUtensorMap tm_b,
@@ -220,7 +291,9 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
 
   const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const uint32_t lane = threadIdx.x & 31;
-  if (p.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) p.trace[8 * 62 + 0] = globaltimer_ns();
+  // DIAGNOSTIC trace: the CTA to trace is read from trace[8 * 63 + 7] (0 = CTA 0)
+  const bool trace_me = p.trace != nullptr && blockIdx.x == static_cast<unsigned>(p.trace[8 * 63 + 7]);
+  if (trace_me && threadIdx.x == 0) p.trace[8 * 62 + 0] = globaltimer_ns();
   constexpr int MC = Cfg::MC;
   const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
   // A multicast (MC > 1): the MC CTAs of a cluster own tiles (tm, MC * tg + r), r = rank
@@ -256,10 +329,11 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   // overlapped the previous grid's tail; no global memory is touched before this
   // (bar the diagnostic trace stamps)
   griddep_wait();
-  if (p.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) p.trace[8 * 62 + 1] = globaltimer_ns();
+  if (trace_me && threadIdx.x == 0) p.trace[8 * 62 + 1] = globaltimer_ns();
 
   const int cluster = static_cast<int>(blockIdx.x) / (CG * MC);
   const int nclusters = static_cast<int>(gridDim.x) / (CG * MC);
+  const Work work = work_of<SK>(p, cluster, nclusters);
 
   if (warp == Cfg::W_PRODUCER) {
     // ===================== TMA producer =====================
@@ -270,15 +344,17 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
+      for (; it < work.n_items; ++it) {
+        const Item itm = item_of<SK>(p, work, cluster, nclusters, it);
+        const int tile = itm.tile;
         int tm, tn;
         tile_coords(tile, p, tm, tn);
         if constexpr (MC > 1) tn = MC * tn + static_cast<int>(mrank);
         const int a_row = tm * BM * CG + static_cast<int>(rank) * BM;
         const int b_col = tn * BN + static_cast<int>(rank) * Cfg::BN_CTA;
-        const bool backwards = p.k_serpentine && (it & 1);
-        if (tile + nclusters >= p.num_tiles) griddep_launch_dependents();   // last tile: let the next grid ramp
-        if (p.c_row_prefetch == 2 && !p.beta0 && !(p.debug_flags & 2) && tile + nclusters < p.num_tiles) {
+        const bool backwards = !SK && p.k_serpentine && (it & 1);
+        if (it + 1 == work.n_items) griddep_launch_dependents();   // last tile: let the next grid ramp
+        if (!SK && p.c_row_prefetch == 2 && !p.beta0 && !(p.debug_flags & 2) && tile + nclusters < p.num_tiles) {
           // C_in one tile ahead: this CTA's region of the NEXT tile streams into L2
           // under this tile's MMAs, so the epilogue's slot loads hit L2 instead of
           // all SMs fetching from HBM in a burst when their tiles end together
@@ -291,10 +367,10 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
             tma_prefetch_l2_2d(&tm_cpf, ntn * BN + BN / 2, crow + r);
           }
         }
-        for (int kbi = 0; kbi < p.k_blocks; ++kbi) {
+        for (int kbi = itm.kb_lo; kbi < itm.kb_hi; ++kbi) {
           const int kb = backwards ? p.k_blocks - 1 - kbi : kbi;
           mbar_wait(empty_bar + 8 * stage, phase ^ 1u);
-          if ((p.debug_flags & 1) && kbi >= p.ring_stages) {
+          if ((p.debug_flags & 1) && kbi - itm.kb_lo >= p.ring_stages) {
             if (rank == 0) mbar_arrive(full_bar + 8 * stage);
             if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
             continue;
@@ -342,20 +418,22 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       int acc = 0;
       uint32_t acc_phase = 0;
       int it = 0;
-      for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
-        const bool tr = p.trace != nullptr && blockIdx.x == 0 && it < 60;
+      for (; it < work.n_items; ++it) {
+        const Item itm = item_of<SK>(p, work, cluster, nclusters, it);
+        const int n_chunks = SK ? (itm.kb_hi - itm.kb_lo + p.kb_per_chunk - 1) / p.kb_per_chunk : p.k_chunks;
+        const bool tr = trace_me && it < 60;
         uint64_t clk0 = 0;
         if (tr) {
           p.trace[8 * it + 0] = globaltimer_ns();
           clk0 = clock64();
         }
-        for (int ch = 0; ch < p.k_chunks; ++ch) {
+        for (int ch = 0; ch < n_chunks; ++ch) {
           mbar_wait(acce_bar + 8 * acc, acc_phase ^ 1u);
           tc_fence_after();
           if (tr && ch == 0) p.trace[8 * it + 1] = globaltimer_ns();
           const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
-          const int kb0 = ch * p.kb_per_chunk;
-          const int kb1 = min(kb0 + p.kb_per_chunk, p.k_blocks);
+          const int kb0 = itm.kb_lo + ch * p.kb_per_chunk;
+          const int kb1 = min(kb0 + p.kb_per_chunk, itm.kb_hi);
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(full_bar + 8 * stage, phase);
             tc_fence_after();
@@ -378,7 +456,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           }
           if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, 0x3);
           else umma_commit(accf_bar + 8 * acc);
-          if (tr && ch == p.k_chunks - 1) {
+          if (tr && ch == n_chunks - 1) {
             p.trace[8 * it + 2] = globaltimer_ns();
             p.trace[8 * it + 7] = clock64() - clk0;   // SM cycles of this tile (MMA warp)
           }
@@ -408,9 +486,13 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     uint32_t slot_phase = 0;  // bit s = parity to wait for on slot s
     float racc[Cfg::CPW];
     uint64_t t_last = 0, chunk_ns = 0;   // arrival time of the last accumulator, interval
+    bool sig_pending = false;            // stream-K: a token to post once our reduce-adds complete
     int it = 0;
-    for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
-      const bool tr = p.trace != nullptr && blockIdx.x == 0 && ew == 0 && lane == 0 && it < 60;
+    for (; it < work.n_items; ++it) {
+      const Item itm = item_of<SK>(p, work, cluster, nclusters, it);
+      const int tile = itm.tile;
+      const int n_chunks = SK ? (itm.kb_hi - itm.kb_lo + p.kb_per_chunk - 1) / p.kb_per_chunk : p.k_chunks;
+      const bool tr = trace_me && ew == 0 && lane == 0 && it < 60;
       int tm, tn;
       tile_coords(tile, p, tm, tn);
       if constexpr (MC > 1) tn = MC * tn + static_cast<int>(mrank);
@@ -437,8 +519,8 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       // ---- promote each K chunk's TMEM partial sum into F32 registers (RN adds)
       const uint32_t t_lane = tmem_base + ((q * 32u) << 16) + hcol;
 #pragma unroll 1
-      for (int ch = 0; ch < p.k_chunks; ++ch) {
-        if (Cfg::PRE < Cfg::NOUT && ch == p.k_chunks - 1 && lane == 0 && load_c) {
+      for (int ch = 0; ch < n_chunks; ++ch) {
+        if (Cfg::PRE < Cfg::NOUT && ch == n_chunks - 1 && lane == 0 && load_c) {
           // the remaining C_in chunks are needed right after this (last) K chunk:
           // pull them into L2 now, one chunk ahead, so they are neither evicted by
           // a whole tile of operand traffic nor fetched from HBM in a burst.
@@ -448,7 +530,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         if (p.wait_hint_ns) mbar_wait_sleep(accf_bar + 8 * acc, acc_phase, p.wait_hint_ns);
         else mbar_wait(accf_bar + 8 * acc, acc_phase);
         tc_fence_after();
-        if (tr && ch == p.k_chunks - 1) p.trace[8 * it + 4] = globaltimer_ns();
+        if (tr && ch == n_chunks - 1) p.trace[8 * it + 4] = globaltimer_ns();
         if (p.epi_pace) {
           const uint64_t now = globaltimer_ns();
           if (t_last != 0) chunk_ns = now - t_last;
@@ -487,6 +569,11 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       // the tile's last accumulator arrived, so the C traffic of all SMs (whose
       // tiles end together) is spread over half a chunk interval, not a burst.
       const int grow = row0 + static_cast<int>(lane);
+      // last tile, nothing to load: every MMA of this CTA pair has completed (the final
+      // accumulator barrier), so the operand ring is free -- stage all NOUT chunks there
+      // and issue their stores back to back instead of waiting for a slot to be read
+      const bool ring = Cfg::TAIL_RING && p.tail_ring && !load_c && it + 1 == work.n_items;
+      if (ring) fence_proxy_async_smem();
       const uint64_t pace_ns = (p.epi_pace && chunk_ns > 0) ? min(chunk_ns / (2 * Cfg::NOUT), (uint64_t)20000) : 0;
 #pragma unroll
       for (int c = 0; c < Cfg::NOUT; ++c) {
@@ -495,12 +582,14 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           while (globaltimer_ns() < t_go) __nanosleep(256);
         }
         const uint32_t slot = static_cast<uint32_t>(c % Cfg::EPI_SLOTS);
-        const uint32_t sbuf = ebuf0 + slot * Cfg::EPI_BUF;
+        const uint32_t sbuf = ring ? sA + (ew * Cfg::NOUT + c) * Cfg::EPI_BUF : ebuf0 + slot * Cfg::EPI_BUF;
         const uint32_t sbar = ebar0 + 8 * slot;
         const int ccol = col0 + c * Cfg::CW;
         const bool manual = p.c_ragged && (ccol + Cfg::CW > p.N);
-        mbar_wait(sbar, (slot_phase >> slot) & 1u);
-        slot_phase ^= (1u << slot);
+        if (!ring) {
+          mbar_wait(sbar, (slot_phase >> slot) & 1u);
+          slot_phase ^= (1u << slot);
+        }
 #pragma unroll
         for (int j = 0; j < Cfg::RB / 16; ++j) {
           const uint32_t addr = sbuf + swz<Cfg::RB>(lane, static_cast<uint32_t>(j));
@@ -542,6 +631,22 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
+            if (SK && c == 0 && sig_pending) {
+              // the previous item's partial (a tile cluster + 1 finishes): its reduce-adds
+              // were issued a whole drain ago; once they have completed in global memory,
+              // post one token for this warp's region.  Posted here, not right after they
+              // were issued, so the wait for completion never delays this item's drain.
+              bulk_wait_group<0>();
+              fence_proxy_async_global();
+              red_release_gpu_add(p.sk_flags + sk_slot(cluster, rank, ew), 1u);
+              sig_pending = false;
+            }
+            if (SK && c == 0 && itm.wait) {
+              // k-blocks [0, kb_lo) of this tile were added into C by cluster - 1: take
+              // its token before adding ours (fixed order of the two RN adds)
+              take_token(p.sk_flags + sk_slot(cluster - 1, rank, ew));
+              fence_proxy_async_global();
+            }
             if (red) tma_reduce_add_2d_hint(&tm_c, ccol, row0, sbuf, pol_c);
             else tma_store_2d_hint(&tm_c, ccol, row0, sbuf, pol_c);
             // fused all-gather: the same staged chunk goes to every peer's C
@@ -575,7 +680,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
             }
           }
         }
-        if (c + Cfg::EPI_SLOTS < Cfg::NOUT && lane == 0) {
+        if (!ring && c + Cfg::EPI_SLOTS < Cfg::NOUT && lane == 0) {
           // refill this slot with chunk c + SLOTS once its store has read it
           bulk_wait_group_read<0>();
           if (load_c) {
@@ -586,10 +691,17 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           }
         }
       }
+      if (SK && itm.signal) sig_pending = true;
       if (tr) p.trace[8 * it + 6] = globaltimer_ns();
     }
-    if (lane == 0) bulk_wait_group<0>();
-    if (p.trace != nullptr && blockIdx.x == 0 && warp == 0 && lane == 0) p.trace[8 * 62 + 3] = globaltimer_ns();
+    if (lane == 0) {
+      bulk_wait_group<0>();
+      if (SK && sig_pending) {   // (a signalling item that was this CTA's last)
+        fence_proxy_async_global();
+        red_release_gpu_add(p.sk_flags + sk_slot(cluster, rank, ew), 1u);
+      }
+    }
+    if (trace_me && warp == 0 && lane == 0) p.trace[8 * 62 + 3] = globaltimer_ns();
   }
 
   // ===================== teardown =====================
@@ -600,7 +712,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, Cfg::TMEM_COLS);
   }
-  if (p.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) p.trace[8 * 62 + 2] = globaltimer_ns();
+  if (trace_me && threadIdx.x == 0) p.trace[8 * 62 + 2] = globaltimer_ns();
 }
 
 }  // namespace g16

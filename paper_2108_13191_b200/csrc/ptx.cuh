@@ -171,6 +171,27 @@ __device__ __forceinline__ void bulk_wait_group() {
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// Order global-memory accesses of the generic proxy against the async proxy (TMA).
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// Cross-CTA token counters in global memory (stream-K partial-tile hand-over).
+__device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Take one token: wait until the counter is non-zero, then decrement it.
+__device__ __forceinline__ void take_token(unsigned* p) {
+  for (;;) {
+    const unsigned v = ld_acquire_gpu(p);
+    if (v != 0u && atomicCAS(p, v, v - 1u) == v) break;
+    if (v == 0u) __nanosleep(32);
+  }
+}
 
 // ------------------------------------------------------------------ tcgen05
 template <int CG>

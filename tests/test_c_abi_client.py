@@ -35,3 +35,23 @@ def test_c_client_gemm_on_device(tmp_path):
     r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "c_abi_test OK (gpu)" in r.stdout
+
+
+def test_options_struct_layout_matches_header(tmp_path):
+    # the Python binding's ctypes mirror of gemm_options_t must agree with the C header
+    # field by field (size and every offset), or options land in the wrong member
+    fields = [name for name, _ in g._Options._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include "gemm_f16.h"\nint main(void) {\n'
+                   '  printf("size %zu\\n", sizeof(gemm_options_t));\n'
+                   + "".join(f'  printf("{f} %zu\\n", offsetof(gemm_options_t, {f}));\n' for f in fields)
+                   + "  return 0;\n}\n")
+    exe = str(tmp_path / "layout")
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", str(src), "-I", os.path.join(ROOT, "include"), "-o", exe],
+                   check=True, capture_output=True, text=True)
+    got = dict(line.split() for line in subprocess.run([exe], capture_output=True, text=True, check=True)
+               .stdout.splitlines())
+    import ctypes
+    assert int(got["size"]) == ctypes.sizeof(g._Options)
+    for f in fields:
+        assert int(got[f]) == getattr(g._Options, f).offset, f

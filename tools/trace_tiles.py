@@ -10,13 +10,15 @@ A = torch.from_numpy(synth.uniform_f16(0, 0, M, K)).cuda()
 B = torch.from_numpy(synth.uniform_f16(0, 1, K, N)).cuda()
 C = torch.from_numpy((synth.uniform_f32 if mode == "f32" else synth.uniform_f16)(0, 2, M, N)).cuda()
 tr = torch.zeros(512, dtype=torch.int64, device="cuda")
+CTA = int(os.environ.get("TRACE_CTA", "0"))   # CTA to trace (rank 0 of a pair: even)
+tr[8 * 63 + 7] = CTA
 for _ in range(5): g.gemm_f16(A, B, C, **kw)
 g.gemm_f16(A, B, C, trace=tr, **kw)
 torch.cuda.synchronize()
 t = tr.cpu().numpy().reshape(64, 8)
 t0 = t[0, 0]
 e = t[62]
-print(f"CTA0: entry {(e[0]-t0)/1000:.2f} us, setup done {(e[1]-t0)/1000:.2f}, epilogue stores drained {(e[3]-t0)/1000:.2f}, exit {(e[2]-t0)/1000:.2f}")
+print(f"CTA{CTA}: entry {(e[0]-t0)/1000:.2f} us, setup done {(e[1]-t0)/1000:.2f}, epilogue stores drained {(e[3]-t0)/1000:.2f}, exit {(e[2]-t0)/1000:.2f}")
 import time
 torch.cuda.synchronize()
 t_h = time.perf_counter()
