@@ -1,9 +1,9 @@
 #!/bin/bash
-for v in '{"M":300,"N":528,"K":777,"mode":"f16","config":"splitk_128x128_s4","pad":8}' '{"M":200,"N":300,"K":64,"mode":"f16","config":"splitk_128x128_s4"}' '{"M":300,"N":530,"K":1777,"mode":"f32","config":"splitk_128x128_s4","pad":8}'; do
-  for tool in memcheck racecheck synccheck; do
-    timeout 600 compute-sanitizer --tool $tool --error-exitcode 9 python tools/one_launch.py "$v" > gpurun_out/san_$tool.log 2>&1; rc=$?
-    echo "$tool $v rc=$rc $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/san_$tool.log | tr '\n' ' ')"
-  done
-done > gpurun_out/san6.txt
-bash tools/gpu_final2.sh
-cat gpurun_out/san6.txt
+# Round-end evidence after stream-K / tail ring: GPU suite, smoke, default bench, ncu launch list,
+# and the 256-step square sweep with the final pick rules.
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/final3_pytest.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final3_smoke.txt 2>&1
+timeout 600 python bench.py > gpurun_out/final3_bench.json 2> gpurun_out/final3_bench.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final3_bench_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-parity > /dev/null 2>&1
+HI=6144 timeout 900 python tools/sweep256.py > gpurun_out/final3_sweep256.jsonl 2> gpurun_out/final3_sweep256.err
+cat gpurun_out/final3_pytest.txt gpurun_out/final3_smoke.txt
