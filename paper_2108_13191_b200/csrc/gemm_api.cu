@@ -31,8 +31,10 @@ constexpr int kDefaultCRowPrefetch = 0;
 constexpr int kDefaultPdl = 1;   // profiles/r01/findings.md section 9
 constexpr int kDefaultSnake = 0;
 constexpr int kDefaultCReduce = 1;   // findings.md section 14: +1-10 %, bitwise identical
-// stream-K (auto): taken when the last wave of tiles is at most this full, K >= 4096 ...
+// stream-K (auto): taken when the last wave of tiles is at most this full, K >= 4096
+// (F32 C; F16 C: 0.4, where the 256 x 512 tile is the alternative) ...
 constexpr double kStreamKMaxFill = 0.5;
+constexpr double kStreamKMaxFillF16 = 0.4;
 // ... or at most this full with K > 2048 (profiles/r01/stream_k.md: the K = 1024-2048 tiles
 // are too short to pay for the extra partial-tile store phases)
 constexpr double kStreamKMaxFillShortK = 0.3;
@@ -82,12 +84,12 @@ struct ConfigDesc {
   int k_splits = 0;   // split-K configs: CTAs per cluster sharing one tile's K (non-persistent grid)
   int a_mc = 1;       // A-multicast configs: CTAs per cluster sharing A (tiles (tm, a_mc * tg + r))
   int cluster_size() const { return cluster ? cluster : cta_group; }
-  KernelFn sk_fn = nullptr;   // F32 C, stream-K build (CTA-pair tiles only)
+  KernelFn sk_fn[2] = {nullptr, nullptr};   // [acc_type]: the stream-K build (CTA-pair tiles only)
 };
 
 template <class C>
 constexpr KernelFn sk_fn_of() {
-  if constexpr (C::CG == 2 && !C::PEERS && C::MC == 1 && !C::OUT_F16) return &gemm_f16_sm100_kernel<C, true>;
+  if constexpr (C::CG == 2 && !C::PEERS && C::MC == 1) return &gemm_f16_sm100_kernel<C, true>;
   else return nullptr;
 }
 
@@ -97,7 +99,7 @@ constexpr ConfigDesc make_desc() {
                     {C32::SMEM_BYTES, C16::SMEM_BYTES}, {C32::CW, C16::CW}, {C32::RB, C16::RB},
                     {&gemm_f16_sm100_kernel<C32>, &gemm_f16_sm100_kernel<C16>},
                     C32::MC > 1 ? C32::MC : 0, 0, C32::MC,
-                    sk_fn_of<C32>()};
+                    {sk_fn_of<C32>(), sk_fn_of<C16>()}};
 }
 
 template <int BN, int S>
@@ -191,8 +193,8 @@ void init_device(int dev) {
         e = cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(cd.fn[a]), &lc);
         if (e != cudaSuccess || n <= 0) { d.status = GEMM_ERR_CUDA; d.cuda_error = e ? e : cudaErrorInvalidConfiguration; return; }
         d.max_clusters[c][a] = n;
-        if (a == GEMM_ACC_F32 && cd.sk_fn != nullptr) {   // the stream-K build: same smem, same cluster
-          e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.sk_fn),
+        if (cd.sk_fn[a] != nullptr) {   // the stream-K build: same smem, same cluster
+          e = cudaFuncSetAttribute(reinterpret_cast<const void*>(cd.sk_fn[a]),
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, cd.smem[a]);
           if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
         }
@@ -310,6 +312,17 @@ bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void*
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// The stream-K auto rule (profiles/r01/stream_k.md): one to max_waves full waves of pair
+// tiles (beyond that the last wave is a small share of the run; measured up to 7), and a last
+// wave at most kStreamKMaxFill(F16) full with K >= 4096, or at most kStreamKMaxFillShortK
+// full with K > 2048.
+bool stream_k_pays(int64_t tiles, int64_t clusters, int64_t K, int acc_type, int64_t max_waves = 8) {
+  if (clusters <= 0 || tiles < clusters || tiles % clusters == 0 || tiles / clusters > max_waves) return false;
+  const double fill = static_cast<double>(tiles % clusters) / static_cast<double>(clusters);
+  const double max_fill = acc_type == GEMM_ACC_F16 ? kStreamKMaxFillF16 : kStreamKMaxFill;
+  return (K >= 4096 && fill <= max_fill) || (K > 2048 && fill <= kStreamKMaxFillShortK);
+}
+
 // Shape -> configuration (the paper's per-size "best performing version",
 // P:903-905, as a fixed table so results stay deterministic).  Measured on B200
 // (profiles/r01/cfgsweep.md, epilogue_slots.md, graph_small.md, stage_depth.md):
@@ -373,6 +386,11 @@ int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
   // staging slot, and the 6-stage 64-deep ring is best (profiles/r01/f32_short_k_cfg.txt);
   // a ragged N still stages C_in and keeps the second slot of S5
   if (acc_type == GEMM_ACC_F32 && K <= 2048) return N % 4 == 0 ? GEMM_CFG_PAIR_256x256 : GEMM_CFG_PAIR_256x256_S5;
+  // a partial last wave that stream-K spreads over every cluster (F16 C: rather than the
+  // 256 x 512 tile, whose half as many tiles fill waves no better)
+  // (measured against the wide tile up to 4 full waves: 4608^3 -5.5 %, 3840^3 -4 %)
+  if (acc_type == GEMM_ACC_F16 && stream_k_pays(pair_tiles, sm_count / 2, K, acc_type, 4))
+    return GEMM_CFG_PAIR_256x256_K128;
   if (acc_type == GEMM_ACC_F16) {
     // the 256 x 512 tile runs 5-10 % faster per wave under the power cap
     // (profiles/r01/wide_tile.md) but has half as many tiles: take it unless it
@@ -581,19 +599,20 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const int skopt = opts ? opts->stream_k : 0;
   if (skopt < -1 || skopt > 1) return GEMM_ERR_INVALID_VALUE;
   p.sk_tile0 = p.num_tiles;
-  const bool sk_ok = cd.sk_fn != nullptr && a == GEMM_ACC_F32 && n_peers == 0 && p.c_reduce && !p.beta0 &&
-                     p.bias == nullptr && !p.relu && !p.c_ragged && p.debug_flags == 0 && !p.k_serpentine &&
+  // F32 C: the two partials of a split tile meet by reduce-add (needs the reduce-add epilogue);
+  // F16 C: the first part stores C_in + its partial, the second reduce-adds its own (R18)
+  const bool sk_ok = cd.sk_fn[a] != nullptr && n_peers == 0 && (a == GEMM_ACC_F16 || p.c_reduce) && !p.beta0 &&
+                     p.bias == nullptr && !p.relu && !p.accum_f16 && !p.c_ragged && p.debug_flags == 0 &&
+                     !p.k_serpentine &&
                      p.c_row_prefetch != 2 && clusters * 16 <= kSkFlagSlots &&
                      (tiles % clusters + clusters) * static_cast<int64_t>(p.k_blocks) < 0x7fffffffLL;
   const int64_t rem = tiles % clusters, waves = tiles / clusters;
-  const double fill = static_cast<double>(rem) / clusters;
   const bool sk_want = skopt > 0 || (skopt == 0 && !(opts && opts->max_clusters > 0) &&
-                                      ((K >= 4096 && fill <= kStreamKMaxFill) ||
-                                       (K > 2048 && fill <= kStreamKMaxFillShortK)));
+                                      stream_k_pays(tiles, clusters, K, a));
   if (sk_ok && sk_want && waves >= 1 && rem > 0) {
     p.sk_tile0 = static_cast<int>(tiles - rem - clusters);
     p.sk_flags = di.sk_flags;
-    fn = cd.sk_fn;
+    fn = cd.sk_fn[a];
   }
   if (cfg == GEMM_CFG_PAIR_256x512 && (p.bias != nullptr || p.relu || p.accum_f16)) fn = kWideExtFn;
   cudaError_t e = cudaLaunchKernelEx(&lc, fn, tm_a, tm_b, tm_c, p, pm, tm_cpf);

@@ -498,17 +498,23 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       if constexpr (MC > 1) tn = MC * tn + static_cast<int>(mrank);
       const int row0 = tm * BM * CG + static_cast<int>(rank) * BM + static_cast<int>(q) * 32;
       const int col0 = tn * BN + static_cast<int>(hcol);
+      // stream-K with F16 C: the second part of a split tile is added into C (which the first
+      // part already wrote as C_in + its partial, rounded) by an F16 TMA reduce-add of its own
+      // rounded partial -- no C_in load for that item (R18)
+      const bool f16_tail = SK && Cfg::OUT_F16 && itm.wait;
+      const bool load_it = load_c && !f16_tail;
+      const bool red_it = red || f16_tail;
       if (tr) p.trace[8 * it + 3] = globaltimer_ns();
       // C_in for the first PRE output chunks goes straight into the staging slots
       // now, so its latency hides under this tile's MMAs (the slots were freed by
       // the previous tile's stores).
       if (lane == 0) {
-        if (p.c_row_prefetch && load_c) tma_prefetch_l2_2d(&tm_cpf, col0, row0);
+        if (p.c_row_prefetch && load_it) tma_prefetch_l2_2d(&tm_cpf, col0, row0);
         bulk_wait_group_read<0>();
 #pragma unroll
         for (int c = 0; c < Cfg::PRE; ++c) {
           const uint32_t sbar = ebar0 + 8 * c;
-          if (load_c) {
+          if (load_it) {
             mbar_arrive_expect_tx(sbar, 32 * Cfg::RB);
             tma_load_2d_hint(ebuf0 + c * Cfg::EPI_BUF, &tm_c, col0 + c * Cfg::CW, row0, sbar, pol_c);
           } else {
@@ -520,7 +526,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       const uint32_t t_lane = tmem_base + ((q * 32u) << 16) + hcol;
 #pragma unroll 1
       for (int ch = 0; ch < n_chunks; ++ch) {
-        if (Cfg::PRE < Cfg::NOUT && ch == n_chunks - 1 && lane == 0 && load_c) {
+        if (Cfg::PRE < Cfg::NOUT && ch == n_chunks - 1 && lane == 0 && load_it) {
           // the remaining C_in chunks are needed right after this (last) K chunk:
           // pull them into L2 now, one chunk ahead, so they are neither evicted by
           // a whole tile of operand traffic nor fetched from HBM in a burst.
@@ -572,7 +578,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       // last tile, nothing to load: every MMA of this CTA pair has completed (the final
       // accumulator barrier), so the operand ring is free -- stage all NOUT chunks there
       // and issue their stores back to back instead of waiting for a slot to be read
-      const bool ring = Cfg::TAIL_RING && p.tail_ring && !load_c && it + 1 == work.n_items;
+      const bool ring = Cfg::TAIL_RING && p.tail_ring && !load_it && it + 1 == work.n_items;
       if (ring) fence_proxy_async_smem();
       const uint64_t pace_ns = (p.epi_pace && chunk_ns > 0) ? min(chunk_ns / (2 * Cfg::NOUT), (uint64_t)20000) : 0;
 #pragma unroll
@@ -599,11 +605,11 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           if constexpr (!Cfg::OUT_F16) {
             const float z = red ? -0.f : 0.f;   // (reduce-add: stage the accumulator itself, -0 kept)
             float4 ci = make_float4(z, z, z, z);
-            if (load_c) ci = lds128(addr);
+            if (load_it) ci = lds128(addr);
             o[0] = ci.x + a[0]; o[1] = ci.y + a[1]; o[2] = ci.z + a[2]; o[3] = ci.w + a[3];
           } else {
             uint4 ci = make_uint4(0u, 0u, 0u, 0u);
-            if (!p.beta0) ci = lds128u(addr);
+            if (load_it) ci = lds128u(addr);
             const float2 c0 = f16x2_to_f32(ci.x), c1 = f16x2_to_f32(ci.y);
             const float2 c2 = f16x2_to_f32(ci.z), c3 = f16x2_to_f32(ci.w);
             o[0] = c0.x + a[0]; o[1] = c0.y + a[1]; o[2] = c1.x + a[2]; o[3] = c1.y + a[3];
@@ -647,7 +653,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
               take_token(p.sk_flags + sk_slot(cluster - 1, rank, ew));
               fence_proxy_async_global();
             }
-            if (red) tma_reduce_add_2d_hint(&tm_c, ccol, row0, sbuf, pol_c);
+            if (red_it) tma_reduce_add_2d_hint(&tm_c, ccol, row0, sbuf, pol_c);
             else tma_store_2d_hint(&tm_c, ccol, row0, sbuf, pol_c);
             // fused all-gather: the same staged chunk goes to every peer's C
             if constexpr (Cfg::PEERS)
@@ -683,7 +689,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         if (!ring && c + Cfg::EPI_SLOTS < Cfg::NOUT && lane == 0) {
           // refill this slot with chunk c + SLOTS once its store has read it
           bulk_wait_group_read<0>();
-          if (load_c) {
+          if (load_it) {
             mbar_arrive_expect_tx(sbar, 32 * Cfg::RB);
             tma_load_2d_hint(sbuf, &tm_c, ccol + Cfg::EPI_SLOTS * Cfg::CW, row0, sbar, pol_c);
           } else {

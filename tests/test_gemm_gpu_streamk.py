@@ -49,13 +49,14 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("acc", ["f32", "f16"])
 @pytest.mark.parametrize("cfg", PAIRS)
 @pytest.mark.parametrize("M,N,K,mc", CASES)
-def test_stream_k_parity(g, cfg, M, N, K, mc):
-    A, B, C, gA, gB, gC = device_problem(M, N, K, "f32", seed=M + K, pad=(8, 8, 4))
+def test_stream_k_parity(g, cfg, M, N, K, mc, acc):
+    A, B, C, gA, gB, gC = device_problem(M, N, K, acc, seed=M + K, pad=(8, 8, 8))
     _run(g, gA, gB, gC, config=cfg, max_clusters=mc, stream_k=1)
     ex, _ = oracle_full(A, B, C)
-    check(gC.result(), ex, A, B, "f32", K, f"{cfg} {M}x{N}x{K} clusters={mc} stream-K")
+    check(gC.result(), ex, A, B, acc, K, f"{cfg} {acc} {M}x{N}x{K} clusters={mc} stream-K")
     assert gC.guard_intact() and gA.guard_intact() and gB.guard_intact()
 
 
@@ -77,6 +78,26 @@ def test_stream_k_every_unit_once_exact(g, cfg, mc):
     assert gC.guard_intact()
 
 
+@pytest.mark.parametrize("cfg", ["pair_256x256", "pair_256x256_k128"])
+@pytest.mark.parametrize("mc", [2, 3, 5])
+def test_stream_k_f16_every_unit_once_exact(g, cfg, mc):
+    # F16 C (R18: the second part of a split tile is reduce-added in F16): small integers
+    # with |C| <= 2048 are exact in every rounding, so the result is exact
+    rng = np.random.default_rng(100 + mc)
+    M, N, K = 1100, 1304, 1500
+    Ai = rng.integers(-1, 2, size=(M, K))
+    Bi = rng.integers(-1, 2, size=(K, N))
+    Ci = rng.integers(-100, 101, size=(M, N))
+    exact = Ai @ Bi + Ci
+    assert np.abs(exact).max() <= 2048
+    gA = Guarded(Ai.astype(np.float16), round_up(K, 8))
+    gB = Guarded(Bi.astype(np.float16), round_up(N, 8))
+    gC = Guarded(Ci.astype(np.float16), round_up(N, 8))
+    _run(g, gA, gB, gC, config=cfg, max_clusters=mc, stream_k=1)
+    assert np.array_equal(gC.result().astype(np.int64), exact)
+    assert gC.guard_intact()
+
+
 def test_stream_k_bitwise_repeatable(g):
     # the two reduce-adds of a split tile happen in a fixed order: 6 launches agree
     # bitwise (a token left behind by one launch would let a later one skip its wait)
@@ -92,6 +113,15 @@ def test_stream_k_bitwise_repeatable(g):
         assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
     ex, _ = oracle_full(A, B, C)
     check(outs[0], ex, A, B, "f32", K, "stream-K repeat")
+    # F16 C
+    A, B, C, gA, gB, gC = device_problem(M, N, K, "f16", seed=11)
+    outs = []
+    for _ in range(4):
+        gC.full.copy_(torch.from_numpy(gC.full_host.copy()))
+        _run(g, gA, gB, gC, config="pair_256x256_k128", max_clusters=5, stream_k=1)
+        outs.append(gC.result().copy())
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint16), outs[0].view(np.uint16))
 
 
 def test_stream_k_off_and_on_agree_to_rounding(g):

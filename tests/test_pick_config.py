@@ -26,6 +26,10 @@ CASES = [
     (2048, 2048, 8192, 0, "pair_256x256_k128"),      # ... but not at K = 8192
     (2560, 2048, 2048, 0, "pair_256x256"),           # 80 pair tiles: more than one wave
     (3072, 3072, 2048, 1, "pair_256x512"),
+    (2304, 2304, 2304, 1, "pair_256x256_k128"),      # F16: stream-K over the partial last wave
+    (2560, 2560, 8192, 1, "pair_256x256_k128"),
+    (4608, 4608, 4608, 1, "pair_256x256_k128"),
+    (4096, 4096, 4096, 0, "pair_256x256_k128"),      # F32 (stream-K is decided at launch)
     (32768, 1024, 4096, 1, "pair_256x256_k128"),
     (16384, 4096, 1024, 0, "pair_256x256"),          # F32 one K chunk, reduce-add epilogue
     (8192, 1002, 1000, 0, "pair_256x256_s5"),        # ... but a ragged N (N % 4 != 0) still stages C_in
