@@ -404,6 +404,13 @@ int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
   return GEMM_CFG_PAIR_256x256_K128;
 }
 
+// L2 promotion of an A/B operand map: 256 B when its rows start on 128-byte lines; when
+// they do not (ld * 2 % 128 != 0), every 128-byte box row straddles two lines and the
+// 128 B promotion is faster (8192x1000x1000 +6-10 %, 4104^3 +11-14 %; profiles/r01/findings.md 18)
+CUtensorMapL2promotion operand_promotion(int64_t ld) {
+  return (ld * 2) % 128 == 0 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 gemm_status_t cuda_fail(cudaError_t e) {
@@ -467,9 +474,8 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (bias && !aligned16(bias)) return GEMM_ERR_MISALIGNED;
   CUtensorMap tm_a, tm_b, tm_c;
   const bool ok =
-      encode_2d(&tm_a, in_dt, 2, A, M, K, lda, 64, static_cast<uint32_t>(128 / cd.a_mc),
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
-      encode_2d(&tm_b, in_dt, 2, B, K, N, ldb, 64, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
+      encode_2d(&tm_a, in_dt, 2, A, M, K, lda, 64, static_cast<uint32_t>(128 / cd.a_mc), operand_promotion(lda)) &&
+      encode_2d(&tm_b, in_dt, 2, B, K, N, ldb, 64, 64, operand_promotion(ldb)) &&
       encode_2d(&tm_c, acc_type == GEMM_ACC_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                 acc_type == GEMM_ACC_F32 ? 4 : 2, C, M, N, ldc, static_cast<uint32_t>(cd.c_box_cols[a]),
                 cd.k_splits ? 128 : 32,   // split-K: whole 128-row boxes for the reduce-add steps
