@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -40,7 +41,9 @@ constexpr double kStreamKMaxFillF16 = 0.4;
 constexpr double kStreamKMaxFillShortK = 0.3;
 
 // token counters of the stream-K hand-over (gemm_sm100.cuh): every launch leaves them at
-// zero (each posted token is taken), so no per-launch reset and no allocation is needed
+// zero (each posted token is taken), so no per-launch reset and no allocation is needed.
+// Successive launches take successive windows of the pool, so GEMMs running concurrently on
+// different streams do not share counters (up to ~50 launches in flight at 74 clusters).
 __device__ unsigned g_sk_flags[kSkFlagSlots];
 
 thread_local int t_last_cuda_error = 0;
@@ -155,6 +158,7 @@ struct DeviceInfo {
   int sm_count = 0;
   int max_clusters[GEMM_CFG_COUNT + 1][2] = {};   // [GEMM_CFG_COUNT] = the gather config
   unsigned* sk_flags = nullptr;                    // this device's g_sk_flags
+  std::atomic<uint32_t> sk_next{0};                // next window of the pool
 };
 std::once_flag g_dev_once[kMaxDevices];
 DeviceInfo g_dev[kMaxDevices];
@@ -617,7 +621,10 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
                                       stream_k_pays(tiles, clusters, K, a));
   if (sk_ok && sk_want && waves >= 1 && rem > 0) {
     p.sk_tile0 = static_cast<int>(tiles - rem - clusters);
-    p.sk_flags = di.sk_flags;
+    const uint32_t win = static_cast<uint32_t>(clusters) * 16u;
+    uint32_t base = g_dev[dev].sk_next.fetch_add(win) % kSkFlagSlots;
+    if (base + win > static_cast<uint32_t>(kSkFlagSlots)) base = 0;   // (windows never straddle the end)
+    p.sk_flags = di.sk_flags + base;
     fn = cd.sk_fn[a];
   }
   if (cfg == GEMM_CFG_PAIR_256x512 && (p.bias != nullptr || p.relu || p.accum_f16)) fn = kWideExtFn;

@@ -119,7 +119,7 @@ struct Item {
 };
 // token counter of (cluster boundary b, CTA rank, epilogue warp): the writer warp and
 // the waiting warp cover the same 32 x BN/2 region of the shared tile
-constexpr int kSkFlagSlots = 4096;
+constexpr int kSkFlagSlots = 1 << 16;   // the device pool; each launch takes a window of it
 __device__ __forceinline__ int sk_slot(int b, uint32_t rank, uint32_t ew) {
   return (b * 2 + static_cast<int>(rank)) * 8 + static_cast<int>(ew);
 }
