@@ -101,7 +101,9 @@ typedef struct {
   int promote_k;    /* K elements per TMEM accumulation chunk before the partial sum is  */
                     /* added into F32 registers (RN): 0 = default 2048, -1 = never       */
                     /* (one TMEM chain per tile), else a positive multiple of the        */
-                    /* config's K stage depth (64, or 128 for PAIR_256x256_K128)          */
+                    /* config's K stage depth (64, or 128 for PAIR_256x256_K128).  With   */
+                    /* config AUTO a positive value steers the choice away from the       */
+                    /* split-K and PAIR_256x512 kernels (one chain per CTA by design)     */
   int epi_pace;     /* 0: default (off); 1: pace each tile's C traffic over half a K-chunk */
                     /* interval; -1: off                                                  */
   int ring_stages;  /* 0: all stages of the config; 1..stages: use a shallower smem ring   */

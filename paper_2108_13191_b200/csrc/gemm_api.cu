@@ -464,7 +464,16 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
 
   int cfg = opts ? opts->config : GEMM_CFG_AUTO;
   if (cfg < 0 || cfg >= GEMM_CFG_COUNT) return GEMM_ERR_INVALID_VALUE;
-  if (cfg == GEMM_CFG_AUTO) cfg = pick_config(M, N, K, acc_type, di.sm_count);
+  if (cfg == GEMM_CFG_AUTO) {
+    cfg = pick_config(M, N, K, acc_type, di.sm_count);
+    // an explicit promote_k asks for chunked promotion, which the split-K and 256 x 512
+    // kernels do not have (one chain per CTA by design): take the closest kernel that has it
+    if (opts && opts->promote_k > 0 && (config_desc(cfg).k_splits || cfg == GEMM_CFG_PAIR_256x512)) {
+      const int64_t pair_tiles = cdiv(M, 256) * cdiv(N, 256);
+      cfg = (M <= 128 || 2 * pair_tiles <= di.sm_count / 2) ? GEMM_CFG_SOLO_128x64
+            : (opts->promote_k % 128 == 0 ? GEMM_CFG_PAIR_256x256_K128 : GEMM_CFG_PAIR_256x256);
+    }
+  }
   if (n_peers > 0) cfg = GEMM_CFG_COUNT;   // fused gather: the peer-store build of PAIR_256x256_K128
   const ConfigDesc& cd = config_desc(cfg);
   const int a = acc_type;

@@ -450,3 +450,17 @@ def test_pdl_dependent_chain_exact(config):
     gr.replay(); gr.replay()
     torch.cuda.synchronize()
     assert torch.equal(C.double(), C0.double() + 8 * AB)
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+@pytest.mark.parametrize("shape,pk", [((44, 76, 1064), 128), ((300, 300, 8192), 256), ((1024, 1024, 4096), 64),
+                                      ((2048, 2048, 2048), 512)])
+def test_auto_with_promote_k_avoids_single_chain_kernels(g, acc, shape, pk):
+    # auto would pick a split-K or 256 x 512 kernel for some of these (one TMEM chain per
+    # CTA, promote_k rejected there); an explicit promote_k steers auto to a kernel with
+    # chunked promotion instead of failing (found by the fuzz campaign, case 257)
+    M, N, K = shape
+    A, B, C, gA, gB, gC = device_problem(M, N, K, acc, seed=K, pad=(8, 8, 8))
+    _run(g, gA, gB, gC, promote_k=pk)
+    ex, _ = oracle_full(A, B, C)
+    check(gC.result(), ex, A, B, acc, K, f"auto promote_k={pk} {shape}")

@@ -1,6 +1,6 @@
 """Seeded fuzzing of the CUDA path against the oracle: random shapes (incl. 1 and
 odd sizes), random padded leading dims, random configurations and scheduling /
-epilogue options, both output modes and both input types; guard bands must stay
+epilogue options (stream-K included), both output modes and both input types; guard bands must stay
 untouched.  Every case is reproducible from its index."""
 import os
 
@@ -24,7 +24,10 @@ def _guarded_dev(host_bits, ld, rows_extra, canary):
     return full, torch.from_numpy(full.copy()).cuda()
 
 
-@pytest.mark.parametrize("case", range(48))
+N_MAIN = int(os.environ.get("FUZZ_MAIN", "48"))    # a longer campaign: FUZZ_MAIN=500
+
+
+@pytest.mark.parametrize("case", range(N_MAIN))
 def test_fuzz_against_oracle(case):
     _fuzz_case(case, 10_000 + case, wide=False)
 
@@ -87,6 +90,8 @@ def _fuzz_case(case, seed, wide, configs=None):
     lda = round_up(max(K, 1), 8) + 8 * int(rng.integers(0, 3))
     ldb = round_up(max(N, 1), 8) + 8 * int(rng.integers(0, 3))
     ldc = round_up(max(N, 1), 16 // csz) + (16 // csz) * int(rng.integers(0, 3))
+    if not wide and rng.random() < 0.4:
+        kw["stream_k"] = 1        # pair configs with a partial last wave split tiles (else ignored)
     _, dA = _guarded_dev(Abits, lda, 1, np.uint16(CANARY_F16))
     _, dB = _guarded_dev(Bbits, ldb, 1, np.uint16(CANARY_F16))
     cbits = C.view(np.uint32 if acc == "f32" else np.uint16)
