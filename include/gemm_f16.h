@@ -150,7 +150,8 @@ typedef struct {
                     /* -1 = off                                                             */
   int tail_ring;    /* 0: default (on); -1: off.  On a CTA's last tile, when no C_in is     */
                     /* staged, all output chunks are staged at once in the idle operand    */
-                    /* ring and stored back to back (256x256-class pair and 1-CTA configs) */
+                    /* ring and stored back to back (256x256-class pair, 1-CTA and        */
+                    /* PAIR_256x512 configs)                                               */
 } gemm_options_t;
 
 /*

@@ -356,24 +356,31 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
       }
       acc_phase ^= 1u;
       if (tr) p.trace[8 * it + 5] = globaltimer_ns();
-      // ---- C_out: registers -> swizzled staging -> TMA store (overlaps the next mainloop)
+      // ---- C_out: registers -> swizzled staging -> TMA store (overlaps the next mainloop).
+      // Last tile: every MMA of the pair has completed (both halves' barriers), so the
+      // operand ring is idle -- stage all NOUT chunks there and store them back to back
+      // (static_assert below: 8 warps x NOUT x 4 KB fit in the ring)
+      static_assert(Cfg::EPI_WARPS * Cfg::NOUT * Cfg::EPI_BUF <= Cfg::STAGES * Cfg::STAGE_BYTES, "tail ring");
+      const bool ring = p.tail_ring && tile + nclusters >= p.num_tiles;
+      if (ring) fence_proxy_async_smem();
       const int grow = row0 + static_cast<int>(lane);
 #pragma unroll
       for (int c = 0; c < Cfg::NOUT; ++c) {
         const int ccol = wide_col(tn, grp, c * Cfg::CW);
         if (ccol >= p.N) break;   // warp-uniform; chunk columns increase with c
-        if (lane == 0) bulk_wait_group_read<0>();
+        const uint32_t sbuf = ring ? sA + (warp * Cfg::NOUT + c) * Cfg::EPI_BUF : ebuf;
+        if (lane == 0 && !ring) bulk_wait_group_read<0>();
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          sts128u(ebuf + swz<128>(lane, static_cast<uint32_t>(j)), cv[32 * c + 4 * j + 0], cv[32 * c + 4 * j + 1],
+          sts128u(sbuf + swz<128>(lane, static_cast<uint32_t>(j)), cv[32 * c + 4 * j + 0], cv[32 * c + 4 * j + 1],
                   cv[32 * c + 4 * j + 2], cv[32 * c + 4 * j + 3]);
         const bool manual = p.c_ragged && (ccol + Cfg::CW > p.N);
         if (!manual) {
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d_hint(&tm_c, ccol, row0, ebuf, pol_c);
+            tma_store_2d_hint(&tm_c, ccol, row0, sbuf, pol_c);
             bulk_commit_group();
           }
         } else {
@@ -384,7 +391,7 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
             uint16_t* dst = static_cast<uint16_t*>(p.c_ptr) + static_cast<long long>(grow) * p.ldc;
 #pragma unroll 1
             for (int j = 0; j < 8; ++j) {
-              const uint4 v = lds128u(ebuf + swz<128>(lane, static_cast<uint32_t>(j)));
+              const uint4 v = lds128u(sbuf + swz<128>(lane, static_cast<uint32_t>(j)));
               const uint32_t o[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
               for (int e = 0; e < 8; ++e)
