@@ -320,8 +320,13 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // tiles (beyond that the last wave is a small share of the run; measured up to 7), and a last
 // wave at most kStreamKMaxFill(F16) full with K >= 4096, or at most kStreamKMaxFillShortK
 // full with K > 2048.
+// Below one wave (half to 70 % of the clusters have a tile) every tile is shared out; that
+// pays only with long K (F16 K >= 4096, F32 K >= 8192: 1792^2 x 8192 -15 % F16, -7 % F32;
+// profiles/r01/stream_k.md, one-wave section).
 bool stream_k_pays(int64_t tiles, int64_t clusters, int64_t K, int acc_type, int64_t max_waves = 8) {
-  if (clusters <= 0 || tiles < clusters || tiles % clusters == 0 || tiles / clusters > max_waves) return false;
+  if (clusters > 0 && tiles < clusters)
+    return 2 * tiles >= clusters && 10 * tiles <= 7 * clusters && K >= (acc_type == GEMM_ACC_F16 ? 4096 : 8192);
+  if (clusters <= 0 || tiles % clusters == 0 || tiles / clusters > max_waves) return false;
   const double fill = static_cast<double>(tiles % clusters) / static_cast<double>(clusters);
   const double max_fill = acc_type == GEMM_ACC_F16 ? kStreamKMaxFillF16 : kStreamKMaxFill;
   return (K >= 4096 && fill <= max_fill) || (K > 2048 && fill <= kStreamKMaxFillShortK);
@@ -578,6 +583,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   int clusters = di.max_clusters[cfg][a];
   if (opts && opts->max_clusters > 0) clusters = opts->max_clusters;
   if (opts && opts->max_clusters < 0) return GEMM_ERR_INVALID_VALUE;
+  const int grid_cap = clusters;   // (stream-K below one wave uses the whole grid)
   clusters = static_cast<int>(std::min<int64_t>(clusters, tiles));
   if (cd.k_splits) clusters = static_cast<int>(tiles);   // one tile per cluster (non-persistent)
 
@@ -623,13 +629,19 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const bool sk_ok = cd.sk_fn[a] != nullptr && n_peers == 0 && (a == GEMM_ACC_F16 || p.c_reduce) && !p.beta0 &&
                      p.bias == nullptr && !p.relu && !p.accum_f16 && !p.c_ragged && p.debug_flags == 0 &&
                      !p.k_serpentine &&
-                     p.c_row_prefetch != 2 && clusters * 16 <= kSkFlagSlots &&
-                     (tiles % clusters + clusters) * static_cast<int64_t>(p.k_blocks) < 0x7fffffffLL;
-  const int64_t rem = tiles % clusters, waves = tiles / clusters;
+                     p.c_row_prefetch != 2 && grid_cap * 16 <= kSkFlagSlots &&
+                     (tiles % grid_cap + grid_cap) * static_cast<int64_t>(p.k_blocks) < 0x7fffffffLL;
+  const int64_t skc = grid_cap;   // stream-K runs on the whole grid
+  const int64_t rem = tiles % skc, waves = tiles / skc;
   const bool sk_want = skopt > 0 || (skopt == 0 && !(opts && opts->max_clusters > 0) &&
-                                      stream_k_pays(tiles, clusters, K, a));
-  if (sk_ok && sk_want && waves >= 1 && rem > 0) {
-    p.sk_tile0 = static_cast<int>(tiles - rem - clusters);
+                                      stream_k_pays(tiles, skc, K, a));
+  // (less than one wave: every tile is shared out, as long as each cluster gets at least
+  // half a tile of k-blocks, so a tile is split at most three ways and a chain of waits is
+  // at most two long)
+  if (sk_ok && sk_want && rem > 0 && (waves >= 1 || 2 * tiles >= skc)) {
+    clusters = static_cast<int>(skc);
+    lc.gridDim = dim3(static_cast<unsigned>(clusters * cl_size), 1, 1);
+    p.sk_tile0 = waves >= 1 ? static_cast<int>(tiles - rem - clusters) : 0;
     const uint32_t win = static_cast<uint32_t>(clusters) * 16u;
     uint32_t base = g_dev[dev].sk_next.fetch_add(win) % kSkFlagSlots;
     if (base + win > static_cast<uint32_t>(kSkFlagSlots)) base = 0;   // (windows never straddle the end)

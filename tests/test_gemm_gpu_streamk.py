@@ -46,6 +46,9 @@ CASES = [
     (600, 1500, 4200, 4),     # 18 tiles; K crosses two promotion chunks (2048)
     (770, 770, 3000, 3),      # 16 tiles on 3 clusters: 4 stream-K tiles, runs of 62.7 k-blocks (47 per tile)
     (512, 2560, 200, 6),      # short K: 4 / 2 k-blocks per tile
+    (700, 700, 2000, 12),     # fewer tiles (9) than clusters: tiles split up to three ways
+    (600, 1000, 1500, 10),    # 12 tiles on 10 clusters... and 6 on 10 below
+    (300, 1500, 900, 10),
 ]
 
 

@@ -30,6 +30,8 @@ CASES = [
     (2560, 2560, 8192, 1, "pair_256x256_k128"),
     (4608, 4608, 4608, 1, "pair_256x256_k128"),
     (4096, 4096, 4096, 0, "pair_256x256_k128"),      # F32 (stream-K is decided at launch)
+    (1792, 1792, 8192, 1, "pair_256x256_k128"),      # F16 below one wave, long K: stream-K
+    (1792, 1792, 4096, 1, "pair_256x256_s4"),        # (one wave, K <= 4096: the 3-slot config)
     (32768, 1024, 4096, 1, "pair_256x256_k128"),
     (16384, 4096, 1024, 0, "pair_256x256"),          # F32 one K chunk, reduce-add epilogue
     (8192, 1002, 1000, 0, "pair_256x256_s5"),        # ... but a ragged N (N % 4 != 0) still stages C_in
