@@ -91,9 +91,9 @@ struct GemmParams {
   int l2_hints;                     // 1: TMA loads/stores carry L2 eviction-priority hints
                                     // (A evict_last: re-read by the next wave of tiles;
                                     //  C evict_first: streamed once)
-  // stream-K (kernel built with SK = true; F32 C with the reduce-add epilogue only):
-  // tiles [sk_tile0, num_tiles) are shared out as equal runs of (tile, k-block) units, one
-  // run per cluster, so the last partial wave is spread over every cluster
+  // stream-K (kernel built with SK = true; F32 C with the reduce-add epilogue, or F16 C --
+  // DESIGN.md R18): tiles [sk_tile0, num_tiles) are shared out as equal runs of (tile,
+  // k-block) units, one run per cluster, so the last partial wave is spread over every cluster
   int sk_tile0;
   unsigned* sk_flags;               // token counters, one per (cluster boundary, CTA, epilogue warp)
   int tail_ring;                    // 1: the last tile's output chunks are staged all at once in the
@@ -108,7 +108,9 @@ struct GemmParams {
 // its partial into C first and posts a token; c + 1 takes it before adding its own, so the
 // two reduce-adds into C happen in a fixed order (deterministic result), and a cluster
 // only ever waits on a lower-numbered one that did that work first.  The host gives every
-// cluster at least k_blocks units, so a tile is split at most once.
+// cluster at least k_blocks units, so a tile is split at most once -- or, below one wave,
+// at least k_blocks / 2, so a tile is split at most three ways (a middle part waits for
+// cluster - 1 and posts for cluster + 1: chains of waits stay two long).
 struct Work {
   int n_dp, n_items, t_hi;
   int u0, u1;   // (the host keeps the stream-K unit count below 2^31)
