@@ -642,6 +642,9 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
     clusters = static_cast<int>(skc);
     lc.gridDim = dim3(static_cast<unsigned>(clusters * cl_size), 1, 1);
     p.sk_tile0 = waves >= 1 ? static_cast<int>(tiles - rem - clusters) : 0;
+    // run boundaries within k_blocks / 8 of a tile edge snap to it (at least one full wave;
+    // below one wave equal runs matter more: profiles/r01/stream_k.md, snapping)
+    p.sk_snap = waves >= 1 ? p.k_blocks / 8 : 0;
     const uint32_t win = static_cast<uint32_t>(clusters) * 16u;
     uint32_t base = g_dev[dev].sk_next.fetch_add(win) % kSkFlagSlots;
     if (base + win > static_cast<uint32_t>(kSkFlagSlots)) base = 0;   // (windows never straddle the end)

@@ -95,6 +95,7 @@ struct GemmParams {
   // DESIGN.md R18): tiles [sk_tile0, num_tiles) are shared out as equal runs of (tile,
   // k-block) units, one run per cluster, so the last partial wave is spread over every cluster
   int sk_tile0;
+  int sk_snap;                      // run boundaries within this many k-blocks of a tile edge snap to it
   unsigned* sk_flags;               // token counters, one per (cluster boundary, CTA, epilogue warp)
   int tail_ring;                    // 1: the last tile's output chunks are staged all at once in the
                                     // (then idle) operand ring instead of cycling through the slots
@@ -125,6 +126,15 @@ constexpr int kSkFlagSlots = 1 << 16;   // the device pool; each launch takes a 
 __device__ __forceinline__ int sk_slot(int b, uint32_t rank, uint32_t ew) {
   return (b * 2 + static_cast<int>(rank)) * 8 + static_cast<int>(ew);
 }
+// A run boundary that falls within `snap` k-blocks of a tile edge moves onto the edge: no
+// sliver of a tile is split off, which would cost a whole extra store phase for a few
+// k-blocks of work (the host keeps snap <= k_blocks / 4, so runs stay >= k_blocks / 2)
+__device__ __forceinline__ int sk_boundary(long long b, int kb, int snap) {
+  const int r = static_cast<int>(b % kb);
+  if (r != 0 && r < snap) return static_cast<int>(b - r);
+  if (r != 0 && kb - r < snap) return static_cast<int>(b - r + kb);
+  return static_cast<int>(b);
+}
 template <bool SK>
 __device__ __forceinline__ Work work_of(const GemmParams& p, int cluster, int ncl) {
   Work w;
@@ -135,8 +145,8 @@ __device__ __forceinline__ Work work_of(const GemmParams& p, int cluster, int nc
   w.u0 = w.u1 = 0;
   if constexpr (SK) {
     const long long units = static_cast<long long>(p.num_tiles - p.sk_tile0) * p.k_blocks;
-    w.u0 = static_cast<int>(units * cluster / ncl);
-    w.u1 = static_cast<int>(units * (cluster + 1) / ncl);
+    w.u0 = sk_boundary(units * cluster / ncl, p.k_blocks, p.sk_snap);
+    w.u1 = sk_boundary(units * (cluster + 1) / ncl, p.k_blocks, p.sk_snap);
     if (w.u1 > w.u0) {
       w.t_hi = (w.u1 - 1) / p.k_blocks;
       w.n_items += w.t_hi - w.u0 / p.k_blocks + 1;
