@@ -139,15 +139,16 @@ typedef struct {
                     /* adds its tile into C with a TMA reduce-add store instead of loading */
                     /* C_in into shared memory (bitwise the same single RN add); -1 = off; */
                     /* 0 = default (on)                                                     */
-  int stream_k;     /* CTA-pair configs, no bias/ReLU/beta=0/ragged N (F32 C: reduce-add     */
-                    /* epilogue; F16 C: DESIGN R18): 1 = when the last                      */
-                    /* wave of tiles is partial, share the last partial wave plus one full  */
-                    /* wave out over all clusters as equal runs of k-blocks (split tiles    */
-                    /* meet in C by two reduce-adds in a fixed order; deterministic for a   */
-                    /* given grid); 0 = default (on when max_clusters is 0 and the last     */
-                    /* wave is <= 50 % (F16 C: 40 %) full with K >= 4096, or <= 30 % full   */
-                    /* with K > 2048);                                                      */
-                    /* -1 = off                                                             */
+  int stream_k;     /* CTA-pair 256x256 configs, no bias/ReLU/beta=0/ragged N (F32 C:       */
+                    /* reduce-add epilogue; F16 C: DESIGN R18).  1 = when the last wave of  */
+                    /* tiles is partial, share the last partial wave plus one full wave     */
+                    /* (below one wave: every tile) out over all clusters as equal runs of  */
+                    /* k-blocks; the parts of a split tile meet in C in a fixed order (F32: */
+                    /* reduce-adds; F16: a store, then an F16 reduce-add), so results are   */
+                    /* deterministic for a given grid.  0 = default: on when max_clusters   */
+                    /* is 0 and stream-K pays (1-8 full waves with the last <= 50 % full,   */
+                    /* F16 40 %, for K >= 4096 or <= 30 % for K > 2048; below one wave,     */
+                    /* 50-70 % of the clusters busy and K >= 4096 F16 / 8192 F32).  -1 = off */
   int tail_ring;    /* 0: default (on); -1: off.  On a CTA's last tile, when no C_in is     */
                     /* staged, all output chunks are staged at once in the idle operand    */
                     /* ring and stored back to back (256x256-class pair, 1-CTA and        */
