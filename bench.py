@@ -157,11 +157,20 @@ def oracle_sample_rate(n: int, modes, budget_s: float, seed: int = 0):
     # OpenMP runs one row per thread, so the cost grows in rounds of `threads`
     # rows: time one full round, then take as many rounds as fit the budget.
     threads = max(1, oracle.num_threads())
-    t0 = time.perf_counter()
-    for m in modes:
-        oracle.gemm(A, B, Cs[m], rows=np.arange(min(n, threads)))
-    t_round = max(time.perf_counter() - t0, 1e-6)
-    rows = int(min(n, max(1, int(budget_s / t_round)) * threads))
+
+    def timed_rounds(k):
+        t0 = time.perf_counter()
+        for m in modes:
+            oracle.gemm(A, B, Cs[m], rows=np.arange(min(n, k * threads)))
+        return time.perf_counter() - t0
+
+    # per-call cost (argument marshalling of the n x n inputs) + per-round cost: time one
+    # and three rounds (after a warm-up call) and fit both, so the sample fills the budget
+    timed_rounds(1)
+    t1, t3 = timed_rounds(1), timed_rounds(3)
+    t_round = max((t3 - t1) / 2, 1e-6)
+    t_call = max(t1 - t_round, 0.0)
+    rows = int(min(n, max(1, int(max(budget_s - t_call, t_round) / t_round)) * threads))
     sel = np.linspace(0, n - 1, rows).astype(np.int64)
     t0 = time.perf_counter()
     for m in modes:
