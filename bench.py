@@ -200,11 +200,20 @@ def run_reference(args):
     total_budget = 150.0
     per_step = total_budget / max(1, args.steps + args.warmup)
     threads = max(1, oracle.num_threads())
-    t0 = time.perf_counter()
-    for m in modes:
-        oracle.gemm(A, B, Cs[m], rows=np.arange(min(n, threads)))
-    t_round = max(time.perf_counter() - t0, 1e-6)
-    rows = int(min(n, max(1, int(per_step / t_round)) * threads))
+
+    def timed_rounds(k):
+        t0 = time.perf_counter()
+        for m in modes:
+            oracle.gemm(A, B, Cs[m], rows=np.arange(min(n, k * threads)))
+        return time.perf_counter() - t0
+
+    # per-call + per-round cost fitted from one and three rounds (as in oracle_sample_rate)
+    timed_rounds(1)
+    t1, t3 = timed_rounds(1), timed_rounds(3)
+    t_round = max((t3 - t1) / 2, 1e-6)
+    t_call = max(t1 - t_round, 0.0)
+    # (0.75: margin for the fit, so the whole run stays within ~total_budget)
+    rows = int(min(n, max(1, int(max(0.75 * per_step - t_call, t_round) / t_round)) * threads))
     sel = np.linspace(0, n - 1, rows).astype(np.int64)
     for _ in range(args.warmup):
         for m in modes:
