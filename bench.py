@@ -361,6 +361,27 @@ def main():
         except (OSError, ValueError):
             traffic = None
 
+    # --------------------------------------------------------- SM clock seen by the kernel itself
+    # NVML's clock reading lags over a ~50 ms window; one extra traced launch right after the
+    # burst timed region (not timed; BEFORE the sustained window, so it sees the burst regime)
+    # reports clock64 / globaltimer of CTA 0's MMA warp per tile.
+    kernel_clock = None
+    try:
+        tr = torch.zeros(512, dtype=torch.int64, device=dev)
+        with torch.cuda.stream(stream):
+            step()
+            g.gemm_f16(A, B, C[modes[0]], stream=stream, config=args.config, trace=tr)
+        torch.cuda.synchronize()
+        t = tr.cpu().numpy().reshape(64, 8)
+        ghz = [t[i, 7] / (t[i, 2] - t[i, 0]) for i in range(60) if t[i, 0] and t[i, 2] > t[i, 0] and t[i, 7]]
+        if ghz:
+            kernel_clock = {"sm_mhz_median": round(1000 * float(statistics.median(ghz)), 1),
+                            "sm_mhz_min": round(1000 * float(min(ghz)), 1), "sm_mhz_max": round(1000 * float(max(ghz)), 1),
+                            "tiles": len(ghz), "how": "clock64/globaltimer of CTA 0's MMA warp per tile, one traced "
+                                                      "launch right after the timed region"}
+    except Exception as ex:  # tracing is diagnostic only
+        kernel_clock = {"error": str(ex)[:120]}
+
     # --------------------------------------------------------- sustained (power-capped) regime
     # The main region (~50 ms) is a burst: the board has not yet settled at its
     # power cap and NVML's clock reading lags.  Run the same steps back to back for
@@ -389,26 +410,6 @@ def main():
                      "clocks": sclk.summary(),
                      "note": "same steps back to back for longer, after the main region; peak = MEASURED_PEAKS "
                              "bf16_tflops_sustained (cuBLAS, 4 s back to back)"}
-
-    # --------------------------------------------------------- SM clock seen by the kernel itself
-    # NVML's clock reading lags over a ~50 ms window; one extra traced launch (after the
-    # timed region, not timed) reports clock64 / globaltimer of CTA 0's MMA warp per tile.
-    kernel_clock = None
-    try:
-        tr = torch.zeros(512, dtype=torch.int64, device=dev)
-        with torch.cuda.stream(stream):
-            step()
-            g.gemm_f16(A, B, C[modes[0]], stream=stream, config=args.config, trace=tr)
-        torch.cuda.synchronize()
-        t = tr.cpu().numpy().reshape(64, 8)
-        ghz = [t[i, 7] / (t[i, 2] - t[i, 0]) for i in range(60) if t[i, 0] and t[i, 2] > t[i, 0] and t[i, 7]]
-        if ghz:
-            kernel_clock = {"sm_mhz_median": round(1000 * float(statistics.median(ghz)), 1),
-                            "sm_mhz_min": round(1000 * float(min(ghz)), 1), "sm_mhz_max": round(1000 * float(max(ghz)), 1),
-                            "tiles": len(ghz), "how": "clock64/globaltimer of CTA 0's MMA warp per tile, one traced "
-                                                      "launch right after the timed region"}
-    except Exception as ex:  # tracing is diagnostic only
-        kernel_clock = {"error": str(ex)[:120]}
 
     # --------------------------------------------------------- e2e through the host-buffer C ABI
     e2e = None
@@ -541,8 +542,9 @@ def main():
                            regime="burst: ~50 ms timed window after warm-up; see 'sustained' for the "
                                   "power-capped regime",
                            note="NVML sm_mhz is sampled every 2 ms but lags over a 50 ms window; "
-                                "kernel_measured is the SM clock the GEMM ran at right after it "
-                                "(power-capped, sw_power_cap shows up in the longer 'sustained' window)"),
+                                "kernel_measured is the SM clock one traced GEMM ran at right after the "
+                                "burst region and before the sustained window (power-capped, "
+                                "sw_power_cap shows up in the longer 'sustained' window)"),
             "parity": parity,
             "allgather": gather,
         }

@@ -95,50 +95,22 @@ typedef struct {
                     /* many clusters (capped at the tile count; more than the resident */
                     /* slots gives a non-persistent launch)                            */
   int group_m;      /* 0: default raster group height (tiles); >0: override            */
-  int l2_hints;     /* 0: default; 1: TMA L2 eviction hints on; -1: off                 */
-  int debug_flags;  /* 0 for real work.  DIAGNOSTIC ONLY (results are wrong): 1 = skip   */
-                    /* operand loads after the ring fills, 2 = skip C_in/C_out traffic   */
   int promote_k;    /* K elements per TMEM accumulation chunk before the partial sum is  */
                     /* added into F32 registers (RN): 0 = default 2048, -1 = never       */
                     /* (one TMEM chain per tile), else a positive multiple of the        */
                     /* config's K stage depth (64, or 128 for PAIR_256x256_K128).  With   */
                     /* config AUTO a positive value steers the choice away from the       */
                     /* split-K and PAIR_256x512 kernels (one chain per CTA by design)     */
-  int epi_pace;     /* 0: default (off); 1: pace each tile's C traffic over half a K-chunk */
-                    /* interval; -1: off                                                  */
-  int ring_stages;  /* 0: all stages of the config; 1..stages: use a shallower smem ring   */
-  int acc_bufs;     /* 0 or 2: double-buffered TMEM accumulator; 1: single (no overlap)   */
-  int k_serpentine; /* 0: default; 1: odd persistent iterations walk K backwards (L2      */
-                    /* reuse across waves; the K order then depends on the schedule); -1 off */
-  int wait_hint_ns; /* 0: default; >0: suspend-time hint (ns) for the epilogue warps      */
-                    /* waiting for an accumulator; -1: plain polling                     */
-  int c_row_prefetch; /* 0: default; 1: at tile start each epilogue warp L2-prefetches its */
-                    /* whole C_in region in full rows; 2: ... the NEXT tile's region     */
-                    /* (one tile ahead); -1: off                                         */
   /* Fused epilogue (the paper's fusion motivation):       */
   /*   C <- relu?( beta * C_in + A.B + bias[j] ), one rounding to C's type                */
   int in_type;      /* gemm_in_t: GEMM_IN_F16 (default) or GEMM_IN_BF16 for A and B       */
   int beta0;        /* 0: C += A.B (default); 1: C = A.B (C_in not read)                  */
   int relu;         /* 1: max(x, 0) applied before rounding (NaN propagates)              */
   const void* bias; /* NULL, or device float[N] added to every row (16-byte aligned)      */
-  void* trace;      /* DIAGNOSTIC ONLY, normally NULL: device buffer of 512 uint64 that   */
-                    /* receives per-tile globaltimer stamps of CTA 0 (256x256-class pair  */
-                    /* and 1-CTA kernels: of the CTA whose index the caller put in        */
-                    /* element 511 before the call)                                       */
   int accum_f16;    /* EXPERIMENT, 0 normally: 1 = the tensor core accumulates in binary16 */
                     /* (instruction c_format F16: the paper's literal F16 accumulation,   */
                     /* P:979-980; DESIGN R3/R16).  Partial sums are still promoted into   */
                     /* F32 registers every promote_k (-1: one binary16 chain per tile)    */
-  int pdl;          /* 0: default; 1: programmatic dependent launch (the kernel's prologue */
-                    /* overlaps the previous grid's tail in the stream; it waits for that  */
-                    /* grid before touching global memory); -1: off                        */
-  int raster;       /* 0: default; 1: serpentine raster -- odd groups of group_m tile-rows */
-                    /* walk their column strips right to left, so the B columns the last  */
-                    /* wave of a group used are the first the next group needs; -1: plain */
-  int c_reduce;     /* F32 C, plain C += A.B (no bias/ReLU, N % 4 == 0): 1 = the epilogue   */
-                    /* adds its tile into C with a TMA reduce-add store instead of loading */
-                    /* C_in into shared memory (bitwise the same single RN add); -1 = off; */
-                    /* 0 = default (on)                                                     */
   int stream_k;     /* CTA-pair 256x256 configs, no bias/ReLU/beta=0/ragged N (F32 C:       */
                     /* reduce-add epilogue; F16 C: DESIGN R18).  1 = when the last wave of  */
                     /* tiles is partial, share the last partial wave plus one full wave     */
@@ -149,6 +121,20 @@ typedef struct {
                     /* is 0 and stream-K pays (1-8 full waves with the last <= 50 % full,   */
                     /* F16 40 %, for K >= 4096 or <= 30 % for K > 2048; below one wave,     */
                     /* 50-70 % of the clusters busy and K >= 4096 F16 / 8192 F32).  -1 = off */
+  /* Ablation knobs (the paper's fig:gradual-opts; profiles/r02/ablation.md).  */
+  /* Each 0 = the shipped default; results stay within the parity bars for every value.  */
+  int ring_stages;  /* 0: all stages of the config; 1..stages: use a shallower smem ring   */
+  int acc_bufs;     /* 0 or 2: double-buffered TMEM accumulator; 1: single (no overlap)   */
+  int l2_hints;     /* 0: default; 1: TMA L2 eviction hints on; -1: off                   */
+  int pdl;          /* 0: default; 1: programmatic dependent launch (the kernel's prologue */
+                    /* overlaps the previous grid's tail in the stream; it waits for that  */
+                    /* grid before touching global memory); -1: off                        */
+  int raster;       /* 0: default; 1: serpentine raster -- odd groups of group_m tile-rows */
+                    /* walk their column strips right to left; -1: plain                   */
+  int c_reduce;     /* F32 C, plain C += A.B (no bias/ReLU, N % 4 == 0): 1 = the epilogue   */
+                    /* adds its tile into C with a TMA reduce-add store instead of loading */
+                    /* C_in into shared memory (bitwise the same single RN add); -1 = off; */
+                    /* 0 = default (on)                                                     */
   int tail_ring;    /* 0: default (on); -1: off.  On a CTA's last tile, when no C_in is     */
                     /* staged, all output chunks are staged at once in the idle operand    */
                     /* ring and stored back to back (256x256-class pair, 1-CTA and        */

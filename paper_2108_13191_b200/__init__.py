@@ -47,6 +47,9 @@ EXPORTED_SYMBOLS = ("gemm_f16", "gemm_f16_ex", "gemm_f16_gather", "gemm_f16_host
                     "gemm_f16_pick_config_for",
                     "gemm_f16_config_info", "gemm_f16_last_launches", "gemm_status_string",
                     "gemm_last_cuda_error")
+# include/gemm_f16_diag.h (diagnostic entry points; never change a result)
+DIAG_SYMBOLS = ("gemm_f16_diag_set_trace", "gemm_f16_diag_sk_window_base", "gemm_f16_diag_sk_window_slots",
+                "gemm_f16_diag_sk_pool_slots")
 
 
 class GemmError(RuntimeError):
@@ -60,15 +63,18 @@ class GemmError(RuntimeError):
 
 
 class _Options(ctypes.Structure):
+    """gemm_options_t (include/gemm_f16.h), field for field."""
     _fields_ = [("config", ctypes.c_int), ("max_clusters", ctypes.c_int), ("group_m", ctypes.c_int),
-                ("l2_hints", ctypes.c_int), ("debug_flags", ctypes.c_int), ("promote_k", ctypes.c_int),
-                ("epi_pace", ctypes.c_int), ("ring_stages", ctypes.c_int), ("acc_bufs", ctypes.c_int),
-                ("k_serpentine", ctypes.c_int), ("wait_hint_ns", ctypes.c_int),
-                ("c_row_prefetch", ctypes.c_int), ("in_type", ctypes.c_int), ("beta0", ctypes.c_int),
-                ("relu", ctypes.c_int), ("bias", ctypes.c_void_p), ("trace", ctypes.c_void_p),
-                ("accum_f16", ctypes.c_int), ("pdl", ctypes.c_int), ("raster", ctypes.c_int),
-                ("c_reduce", ctypes.c_int), ("stream_k", ctypes.c_int),
-                ("tail_ring", ctypes.c_int)]
+                ("promote_k", ctypes.c_int), ("in_type", ctypes.c_int), ("beta0", ctypes.c_int),
+                ("relu", ctypes.c_int), ("bias", ctypes.c_void_p), ("accum_f16", ctypes.c_int),
+                ("stream_k", ctypes.c_int), ("ring_stages", ctypes.c_int), ("acc_bufs", ctypes.c_int),
+                ("l2_hints", ctypes.c_int), ("pdl", ctypes.c_int), ("raster", ctypes.c_int),
+                ("c_reduce", ctypes.c_int), ("tail_ring", ctypes.c_int)]
+
+
+# the option keywords of gemm_f16 that map 1:1 onto gemm_options_t ints (0 = default)
+_INT_OPTS = ("max_clusters", "group_m", "promote_k", "stream_k", "ring_stages", "acc_bufs", "l2_hints", "pdl",
+             "raster", "c_reduce", "tail_ring")
 
 
 _lib = None
@@ -113,6 +119,15 @@ def load_library(build_if_missing: bool = True):
     lib.gemm_status_string.argtypes = [ci]
     lib.gemm_last_cuda_error.restype = ci
     lib.gemm_last_cuda_error.argtypes = []
+    lib.gemm_f16_diag_set_trace.restype = ci
+    lib.gemm_f16_diag_set_trace.argtypes = [vp]
+    u32 = ctypes.c_uint32
+    lib.gemm_f16_diag_sk_window_base.restype = u32
+    lib.gemm_f16_diag_sk_window_base.argtypes = [u32]
+    lib.gemm_f16_diag_sk_window_slots.restype = u32
+    lib.gemm_f16_diag_sk_window_slots.argtypes = []
+    lib.gemm_f16_diag_sk_pool_slots.restype = u32
+    lib.gemm_f16_diag_sk_pool_slots.argtypes = []
     _lib = lib
     return lib
 
@@ -152,12 +167,21 @@ def _acc_of(C):
     raise TypeError(f"C must be float32 (F32 accumulate) or float16 (F16), got {C.dtype}")
 
 
-def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int = 0, l2_hints: int = 0,
-             debug_flags: int = 0, promote_k: int = 0, epi_pace: int = 0, ring_stages: int = 0,
-             acc_bufs: int = 0, k_serpentine: int = 0, wait_hint_ns: int = 0, c_row_prefetch: int = 0,
-             beta: int = 1, bias=None, relu: bool = False, trace=None, accum_f16: bool = False,
-             pdl: int = 0, raster: int = 0, c_reduce: int = 0, stream_k: int = 0,
-             tail_ring: int = 0):
+def _check_operands(A, B, C, names=("A", "B", "C")):
+    """Device, dtype and placement checks shared by every entry point (no CPU fallback)."""
+    import torch
+    for name, t in zip(names, (A, B, C)):
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if A.dtype not in (torch.float16, torch.bfloat16) or B.dtype != A.dtype:
+        raise TypeError(f"{names[0]} and {names[1]} must both be torch.float16 or both torch.bfloat16")
+    if A.device != C.device or B.device != C.device:
+        raise ValueError(f"{', '.join(names)} must be on the same CUDA device")
+    return _acc_of(C)
+
+
+def gemm_f16(A, B, C, stream=None, config=0, beta: int = 1, bias=None, relu: bool = False,
+             accum_f16: bool = False, trace=None, **opts):
     """In place: C += A @ B on the GPU (enqueued on `stream`, default: torch's current).
 
     A: (M, K) torch.float16 or torch.bfloat16 CUDA, B: (K, N) of the same dtype,
@@ -165,24 +189,24 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
     strides = leading dims).  Fused epilogue: C <- relu?(beta * C + A @ B + bias),
     beta in {1, 0}, bias an (N,) float32 CUDA tensor.  config: a name in CONFIGS or
     its id (0 = auto).  accum_f16 (EXPERIMENT): the tensor core accumulates in
-    binary16 (DESIGN R16).  Raises GemmError on a non-zero status.
+    binary16 (DESIGN R16).  Further keyword options (each 0 = default): the ints of
+    gemm_options_t named in _INT_OPTS (max_clusters, group_m, promote_k, stream_k and
+    the ablation knobs).  trace (DIAGNOSTIC): a CUDA int64 tensor of 512 elements that
+    receives per-tile timestamps (include/gemm_f16_diag.h).  Raises GemmError on a
+    non-zero status.
     """
     import torch
     lib = load_library()
-    for name, t in (("A", A), ("B", B), ("C", C)):
-        if not t.is_cuda:
-            raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
-    if A.dtype not in (torch.float16, torch.bfloat16) or B.dtype != A.dtype:
-        raise TypeError("A and B must both be torch.float16 or both torch.bfloat16")
+    bad = set(opts) - set(_INT_OPTS)
+    if bad:
+        raise TypeError(f"unknown options {sorted(bad)}")
+    acc = _check_operands(A, B, C)
     in_type = 1 if A.dtype == torch.bfloat16 else 0
     if beta not in (0, 1):
         raise ValueError("beta must be 1 (C += A.B) or 0 (C = A.B)")
     if bias is not None and (bias.dtype != torch.float32 or bias.dim() != 1 or bias.numel() != B.shape[1]
-                             or not bias.is_cuda or bias.stride(0) != 1):
-        raise ValueError("bias must be a contiguous float32 CUDA vector of N elements")
-    if A.device != C.device or B.device != C.device:
-        raise ValueError("A, B and C must be on the same CUDA device")
-    acc = _acc_of(C)
+                             or not bias.is_cuda or bias.stride(0) != 1 or bias.device != C.device):
+        raise ValueError("bias must be a contiguous float32 CUDA vector of N elements on C's device")
     M, K = A.shape
     K2, N = B.shape
     if K2 != K or tuple(C.shape) != (M, N):
@@ -195,21 +219,22 @@ def gemm_f16(A, B, C, stream=None, config=0, max_clusters: int = 0, group_m: int
         ctx.__enter__()
     try:
         sh = _stream_handle(stream, dev)
-        if (cfg == 0 and not max_clusters and not group_m and not l2_hints and not debug_flags and not promote_k
-                and not epi_pace and not ring_stages and not acc_bufs and not k_serpentine and not wait_hint_ns
-                and not c_row_prefetch and trace is None and in_type == 0 and beta == 1 and bias is None
-                and not relu and not accum_f16 and not pdl and not raster and not c_reduce and not stream_k and not tail_ring):
+        if trace is not None:
+            if not (trace.is_cuda and trace.dtype == torch.int64 and trace.numel() >= 512):
+                raise ValueError("trace must be a CUDA int64 tensor of >= 512 elements")
+            lib.gemm_f16_diag_set_trace(trace.data_ptr())
+        if (cfg == 0 and in_type == 0 and beta == 1 and bias is None and not relu and not accum_f16
+                and not any(opts.values())):
             st = lib.gemm_f16(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
                               C.data_ptr(), _ld(C, "C"), acc, sh)
         else:
-            opts = _Options(cfg, int(max_clusters), int(group_m), int(l2_hints), int(debug_flags), int(promote_k),
-                            int(epi_pace), int(ring_stages), int(acc_bufs), int(k_serpentine),
-                            int(wait_hint_ns), int(c_row_prefetch), in_type, 1 - int(beta), int(bool(relu)),
-                            None if bias is None else ctypes.c_void_p(bias.data_ptr()),
-                            None if trace is None else ctypes.c_void_p(trace.data_ptr()), int(bool(accum_f16)),
-                            int(pdl), int(raster), int(c_reduce), int(stream_k), int(tail_ring))
+            o = _Options(config=cfg, in_type=in_type, beta0=1 - int(beta), relu=int(bool(relu)),
+                         bias=None if bias is None else ctypes.c_void_p(bias.data_ptr()),
+                         accum_f16=int(bool(accum_f16)), **{k: int(v) for k, v in opts.items()})
             st = lib.gemm_f16_ex(M, N, K, A.data_ptr(), _ld(A, "A"), B.data_ptr(), _ld(B, "B"),
-                                 C.data_ptr(), _ld(C, "C"), acc, sh, ctypes.byref(opts))
+                                 C.data_ptr(), _ld(C, "C"), acc, sh, ctypes.byref(o))
+        if trace is not None:
+            lib.gemm_f16_diag_set_trace(None)   # (disarm if the call failed before launching)
     finally:
         if ctx is not None:
             ctx.__exit__(None, None, None)
@@ -229,7 +254,9 @@ def gemm_f16_gather(A, B_r, C, n0: int, peers=(), stream=None):
     """
     import torch
     lib = load_library()
-    acc = _acc_of(C)
+    acc = _check_operands(A, B_r, C, names=("A", "B_r", "C"))
+    if A.dtype != torch.float16:
+        raise TypeError("gemm_f16_gather takes binary16 A and B_r")
     M, K = A.shape
     K2, nr = B_r.shape
     if K2 != K or C.shape[0] != M or n0 < 0 or n0 + nr > C.shape[1]:
@@ -262,9 +289,18 @@ def gemm_f16_host(hA, hB, hC, dA, dB, dC, stream=None):
     """
     import torch
     lib = load_library()
-    acc = _acc_of(hC)
+    acc = _check_operands(dA, dB, dC, names=("dA", "dB", "dC"))
+    if dA.dtype != torch.float16:
+        raise TypeError("gemm_f16_host takes binary16 A and B")
+    if hC.dtype != dC.dtype or hC.is_cuda:
+        raise TypeError("hC must be a host tensor of dC's dtype")
+    for name, h, d in (("hA", hA, dA), ("hB", hB, dB)):
+        if h is not None and (h.is_cuda or h.dtype != d.dtype):
+            raise TypeError(f"{name} must be a host tensor of the device scratch's dtype")
     M, K = dA.shape
     _, N = dB.shape
+    if tuple(hC.shape) != (M, N) or tuple(dC.shape) != (M, N) or dB.shape[0] != K:
+        raise ValueError("hC/dC must be (M, N) and dB (K, N) for dA (M, K)")
     pA = 0 if hA is None else hA.data_ptr()
     pB = 0 if hB is None else hB.data_ptr()
     lA = 0 if hA is None else _ld(hA, "hA")

@@ -16,6 +16,7 @@
 #include <mutex>
 
 #include "../../include/gemm_f16.h"
+#include "../../include/gemm_f16_diag.h"
 #include "gemm_sm100.cuh"
 #include "gemm_sm100_wide.cuh"
 #include "gemm_sm100_splitk.cuh"
@@ -25,10 +26,6 @@ namespace {
 using namespace g16;
 
 constexpr int kDefaultL2Hints = 1;
-constexpr int kDefaultEpiPace = 0;
-constexpr int kDefaultKSerpentine = 0;
-constexpr unsigned kDefaultWaitHintNs = 0;
-constexpr int kDefaultCRowPrefetch = 0;
 constexpr int kDefaultPdl = 1;   // profiles/r01/findings.md section 9
 constexpr int kDefaultSnake = 0;
 constexpr int kDefaultCReduce = 1;   // findings.md section 14: +1-10 %, bitwise identical
@@ -42,12 +39,19 @@ constexpr double kStreamKMaxFillShortK = 0.3;
 
 // token counters of the stream-K hand-over (gemm_sm100.cuh): every launch leaves them at
 // zero (each posted token is taken), so no per-launch reset and no allocation is needed.
-// Successive launches take successive windows of the pool, so GEMMs running concurrently on
-// different streams do not share counters (up to ~50 launches in flight at 74 clusters).
+// The pool is cut into kSkWindows fixed windows of kSkWindow slots (16 per cluster, for up to
+// 128 clusters); successive launches take successive windows round robin, so two stream-K
+// GEMMs share counters only if kSkWindows - 1 others were issued between them -- concurrent
+// GEMMs on different streams stay isolated up to kSkWindows in flight.
+constexpr int kSkWindow = 16 * 128;
+constexpr int kSkWindows = kSkFlagSlots / kSkWindow;
+static_assert(kSkWindows * kSkWindow == kSkFlagSlots, "whole windows");
 __device__ unsigned g_sk_flags[kSkFlagSlots];
+uint32_t sk_window_base(uint32_t launch_index) { return (launch_index % kSkWindows) * kSkWindow; }
 
 thread_local int t_last_cuda_error = 0;
 thread_local int t_last_launches = 0;
+thread_local unsigned long long* t_trace = nullptr;   // gemm_f16_diag_set_trace: armed for the next call
 
 using Cfg1F32 = KCfg<2, 256, 6, false>;
 using Cfg1F16 = KCfg<2, 256, 6, true>;
@@ -552,31 +556,18 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const int hints = opts ? opts->l2_hints : 0;
   if (hints < -1 || hints > 1) return GEMM_ERR_INVALID_VALUE;
   p.l2_hints = hints == 0 ? kDefaultL2Hints : (hints > 0 ? 1 : 0);
-  p.debug_flags = opts ? opts->debug_flags : 0;
   p.in_bf16 = in_type == GEMM_IN_BF16;
   p.beta0 = (opts && opts->beta0) ? 1 : 0;
   p.relu = (opts && opts->relu) ? 1 : 0;
   p.accum_f16 = (opts && opts->accum_f16) ? 1 : 0;
   p.bias = bias;
-  p.trace = opts ? static_cast<unsigned long long*>(opts->trace) : nullptr;
-  const int pace = opts ? opts->epi_pace : 0;
-  if (pace < -1 || pace > 1) return GEMM_ERR_INVALID_VALUE;
-  p.epi_pace = pace == 0 ? kDefaultEpiPace : (pace > 0 ? 1 : 0);
+  p.trace = t_trace;
   const int rs = opts ? opts->ring_stages : 0;
   if (rs < 0 || rs > cd.stages) return GEMM_ERR_INVALID_VALUE;
   p.ring_stages = rs == 0 ? cd.stages : rs;
   const int ab = opts ? opts->acc_bufs : 0;
   if (ab < 0 || ab > 2) return GEMM_ERR_INVALID_VALUE;
   p.acc_bufs = ab == 0 ? 2 : ab;
-  const int ks = opts ? opts->k_serpentine : 0;
-  if (ks < -1 || ks > 1) return GEMM_ERR_INVALID_VALUE;
-  p.k_serpentine = ks == 0 ? kDefaultKSerpentine : (ks > 0 ? 1 : 0);
-  const int wh = opts ? opts->wait_hint_ns : 0;
-  if (wh < -1) return GEMM_ERR_INVALID_VALUE;
-  p.wait_hint_ns = wh == 0 ? kDefaultWaitHintNs : (wh < 0 ? 0u : static_cast<unsigned>(wh));
-  const int crp = opts ? opts->c_row_prefetch : 0;
-  if (crp < -1 || crp > 2) return GEMM_ERR_INVALID_VALUE;
-  p.c_row_prefetch = crp == 0 ? kDefaultCRowPrefetch : (crp > 0 ? crp : 0);
 
   // persistent grid: one cluster per resident slot; an explicit max_clusters may
   // also exceed the resident slots (a non-persistent launch, for ablation)
@@ -627,9 +618,8 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   // F32 C: the two partials of a split tile meet by reduce-add (needs the reduce-add epilogue);
   // F16 C: the first part stores C_in + its partial, the second reduce-adds its own (R18)
   const bool sk_ok = cd.sk_fn[a] != nullptr && n_peers == 0 && (a == GEMM_ACC_F16 || p.c_reduce) && !p.beta0 &&
-                     p.bias == nullptr && !p.relu && !p.accum_f16 && !p.c_ragged && p.debug_flags == 0 &&
-                     !p.k_serpentine &&
-                     p.c_row_prefetch != 2 && grid_cap * 16 <= kSkFlagSlots &&
+                     p.bias == nullptr && !p.relu && !p.accum_f16 && !p.c_ragged &&
+                     grid_cap * 16 <= kSkWindow &&
                      (tiles % grid_cap + grid_cap) * static_cast<int64_t>(p.k_blocks) < 0x7fffffffLL;
   const int64_t skc = grid_cap;   // stream-K runs on the whole grid
   const int64_t rem = tiles % skc, waves = tiles / skc;
@@ -645,15 +635,13 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
     // run boundaries within k_blocks / 8 of a tile edge snap to it (at least one full wave;
     // below one wave equal runs matter more: profiles/r01/stream_k.md, snapping)
     p.sk_snap = waves >= 1 ? p.k_blocks / 8 : 0;
-    const uint32_t win = static_cast<uint32_t>(clusters) * 16u;
-    uint32_t base = g_dev[dev].sk_next.fetch_add(win) % kSkFlagSlots;
-    if (base + win > static_cast<uint32_t>(kSkFlagSlots)) base = 0;   // (windows never straddle the end)
-    p.sk_flags = di.sk_flags + base;
+    p.sk_flags = di.sk_flags + sk_window_base(g_dev[dev].sk_next.fetch_add(1u));
     fn = cd.sk_fn[a];
   }
   if (cfg == GEMM_CFG_PAIR_256x512 && (p.bias != nullptr || p.relu || p.accum_f16)) fn = kWideExtFn;
   cudaError_t e = cudaLaunchKernelEx(&lc, fn, tm_a, tm_b, tm_c, p, pm, tm_cpf);
   if (e != cudaSuccess) return cuda_fail(e);
+  t_trace = nullptr;   // (a trace is armed for one launch)
   t_last_launches = 1;
   return GEMM_OK;
 }
@@ -802,6 +790,15 @@ gemm_status_t gemm_f16_config_info(int config, int acc_type, int* tile_m, int* t
 }
 
 int gemm_f16_last_launches(void) { return t_last_launches; }
+
+int gemm_f16_diag_set_trace(void* trace) {
+  t_trace = static_cast<unsigned long long*>(trace);
+  return 0;
+}
+
+uint32_t gemm_f16_diag_sk_window_base(uint32_t launch_index) { return sk_window_base(launch_index); }
+uint32_t gemm_f16_diag_sk_window_slots(void) { return kSkWindow; }
+uint32_t gemm_f16_diag_sk_pool_slots(void) { return kSkFlagSlots; }
 
 const char* gemm_status_string(gemm_status_t s) {
   switch (s) {

@@ -64,19 +64,8 @@ struct GemmParams {
   int n_peers;                      // extra destinations of C_out (0 = plain GEMM)
   void* peer_ptr[kMaxPeers];        // their bases, for the ragged-N store path
   long long ldc;                    // C leading dimension in elements
-  int debug_flags;                  // DIAGNOSTIC ONLY (wrong results): 1 = no operand TMA after
-                                    // the ring is filled once per tile, 2 = no C_in/C_out traffic
-  int c_row_prefetch;               // 1: at tile start, one L2 prefetch per epilogue warp of its
-                                    // whole C_in region (full 32 x CPW rows: long DRAM bursts);
-                                    // 2: the producer prefetches the NEXT tile's C_in region
-  unsigned wait_hint_ns;            // suspend-time hint for the epilogue's accumulator waits
-                                    // (0 = plain polling); the producer/MMA always poll
-  int k_serpentine;                 // 1: odd persistent iterations walk K backwards, so the next
-                                    // wave starts on the k-blocks the last one left hot in L2
   int ring_stages;                  // smem ring depth in use (1..STAGES; ablation of Sec 3.5)
   int acc_bufs;                     // TMEM accumulator buffers in use (2 = epilogue overlaps MMA)
-  int epi_pace;                     // 1: spread each tile's C_in/C_out traffic over half a K-chunk
-                                    // interval instead of a burst synchronised across all SMs
   unsigned long long* trace;        // DIAGNOSTIC ONLY (null normally): per-tile globaltimer stamps
                                     // of CTA 0 (MMA start/end + SM cycles, epilogue drain/store),
                                     // 8 per tile; row 62 = kernel entry/setup/exit
@@ -286,7 +275,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                       const __grid_constant__ CUtensorMap tm_c,
                       const __grid_constant__ GemmParams p,
                       const __grid_constant__ PeerMaps peers,
-                      const __grid_constant__ CUtensorMap tm_cpf) {
+                      const __grid_constant__ CUtensorMap /*C_in slice map: split-K kernels only*/) {
   constexpr int CG = Cfg::CG, BN = Cfg::BN, STAGES = Cfg::STAGES, BM = Cfg::BM, BK = Cfg::BK;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -364,29 +353,9 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         if constexpr (MC > 1) tn = MC * tn + static_cast<int>(mrank);
         const int a_row = tm * BM * CG + static_cast<int>(rank) * BM;
         const int b_col = tn * BN + static_cast<int>(rank) * Cfg::BN_CTA;
-        const bool backwards = !SK && p.k_serpentine && (it & 1);
         if (it + 1 == work.n_items) griddep_launch_dependents();   // last tile: let the next grid ramp
-        if (!SK && p.c_row_prefetch == 2 && !p.beta0 && !(p.debug_flags & 2) && tile + nclusters < p.num_tiles) {
-          // C_in one tile ahead: this CTA's region of the NEXT tile streams into L2
-          // under this tile's MMAs, so the epilogue's slot loads hit L2 instead of
-          // all SMs fetching from HBM in a burst when their tiles end together
-          int ntm, ntn;
-          tile_coords(tile + nclusters, p, ntm, ntn);
-          const int crow = ntm * BM * CG + static_cast<int>(rank) * BM;
-#pragma unroll 1
-          for (int r = 0; r < BM; r += 32) {
-            tma_prefetch_l2_2d(&tm_cpf, ntn * BN, crow + r);
-            tma_prefetch_l2_2d(&tm_cpf, ntn * BN + BN / 2, crow + r);
-          }
-        }
-        for (int kbi = itm.kb_lo; kbi < itm.kb_hi; ++kbi) {
-          const int kb = backwards ? p.k_blocks - 1 - kbi : kbi;
+        for (int kb = itm.kb_lo; kb < itm.kb_hi; ++kb) {
           mbar_wait(empty_bar + 8 * stage, phase ^ 1u);
-          if ((p.debug_flags & 1) && kbi - itm.kb_lo >= p.ring_stages) {
-            if (rank == 0) mbar_arrive(full_bar + 8 * stage);
-            if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
-            continue;
-          }
           if (rank == 0) mbar_arrive_expect_tx(full_bar + 8 * stage, Cfg::STAGE_BYTES * CG);
           const uint32_t fb = full_leader + 8 * stage;
           const uint32_t a_dst = sA + stage * Cfg::A_BYTES;
@@ -485,19 +454,17 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     const uint32_t ebar0 = epi_bar + 8 * Cfg::EPI_SLOTS * ew;
     const uint32_t acce_leader = (CG == 2) ? mapa_shared(acce_bar, 0) : acce_bar;
     const uint64_t pol_c = p.l2_hints ? policy_evict_first() : policy_evict_normal();
-    const bool no_c = (p.debug_flags & 2) != 0;
     // F32 C, plain C += A.B: the staged accumulator is added into C by the TMA unit
     // (cp.reduce.async.bulk .add, one IEEE RN add in L2 -- bitwise the same C_in + acc),
     // so C_in is never loaded into shared memory: half the epilogue's shared-memory
     // traffic and no C_in latency chain (findings.md section 14)
-    const bool red = !Cfg::OUT_F16 && !Cfg::PEERS && !no_c && !p.beta0 && p.c_reduce && p.bias == nullptr &&
-                     !p.relu && !p.c_ragged;
-    const bool load_c = !no_c && !p.beta0 && !red;   // C_in traffic through the staging slots
+    const bool red = !Cfg::OUT_F16 && !Cfg::PEERS && !p.beta0 && p.c_reduce && p.bias == nullptr && !p.relu &&
+                     !p.c_ragged;
+    const bool load_c = !p.beta0 && !red;   // C_in traffic through the staging slots
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t slot_phase = 0;  // bit s = parity to wait for on slot s
     float racc[Cfg::CPW];
-    uint64_t t_last = 0, chunk_ns = 0;   // arrival time of the last accumulator, interval
     bool sig_pending = false;            // stream-K: a token to post once our reduce-adds complete
     int it = 0;
     for (; it < work.n_items; ++it) {
@@ -521,7 +488,6 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       // now, so its latency hides under this tile's MMAs (the slots were freed by
       // the previous tile's stores).
       if (lane == 0) {
-        if (p.c_row_prefetch && load_it) tma_prefetch_l2_2d(&tm_cpf, col0, row0);
         bulk_wait_group_read<0>();
 #pragma unroll
         for (int c = 0; c < Cfg::PRE; ++c) {
@@ -545,15 +511,9 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
 #pragma unroll 1
           for (int c = Cfg::PRE; c < Cfg::NOUT; ++c) tma_prefetch_l2_2d(&tm_c, col0 + c * Cfg::CW, row0);
         }
-        if (p.wait_hint_ns) mbar_wait_sleep(accf_bar + 8 * acc, acc_phase, p.wait_hint_ns);
-        else mbar_wait(accf_bar + 8 * acc, acc_phase);
+        mbar_wait(accf_bar + 8 * acc, acc_phase);
         tc_fence_after();
         if (tr && ch == n_chunks - 1) p.trace[8 * it + 4] = globaltimer_ns();
-        if (p.epi_pace) {
-          const uint64_t now = globaltimer_ns();
-          if (t_last != 0) chunk_ns = now - t_last;
-          t_last = now;
-        }
         const uint32_t t_row = t_lane + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
 #pragma unroll
         for (int c = 0; c < Cfg::CPW / 32; ++c) {
@@ -583,22 +543,14 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       }
       if (tr) p.trace[8 * it + 5] = globaltimer_ns();
       // ---- C_out = C_in + acc (F32 add, one rounding to the output type), TMA store.
-      // Paced: output chunk c starts no earlier than c * chunk_ns / (2 * NOUT) after
-      // the tile's last accumulator arrived, so the C traffic of all SMs (whose
-      // tiles end together) is spread over half a chunk interval, not a burst.
       const int grow = row0 + static_cast<int>(lane);
       // last tile, nothing to load: every MMA of this CTA pair has completed (the final
       // accumulator barrier), so the operand ring is free -- stage all NOUT chunks there
       // and issue their stores back to back instead of waiting for a slot to be read
       const bool ring = Cfg::TAIL_RING && p.tail_ring && !load_it && it + 1 == work.n_items;
       if (ring) fence_proxy_async_smem();
-      const uint64_t pace_ns = (p.epi_pace && chunk_ns > 0) ? min(chunk_ns / (2 * Cfg::NOUT), (uint64_t)20000) : 0;
 #pragma unroll
       for (int c = 0; c < Cfg::NOUT; ++c) {
-        if (pace_ns != 0 && c > 0) {
-          const uint64_t t_go = t_last + c * pace_ns;
-          while (globaltimer_ns() < t_go) __nanosleep(256);
-        }
         const uint32_t slot = static_cast<uint32_t>(c % Cfg::EPI_SLOTS);
         const uint32_t sbuf = ring ? sA + (ew * Cfg::NOUT + c) * Cfg::EPI_BUF : ebuf0 + slot * Cfg::EPI_BUF;
         const uint32_t sbar = ebar0 + 8 * slot;
@@ -645,7 +597,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                     cvt_f16x2_rn(o[6], o[7]));
           }
         }
-        if (!manual && !no_c) {
+        if (!manual) {
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -674,7 +626,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
           }
         } else {
           __syncwarp();
-          if (manual && !no_c && grow < p.M) {
+          if (grow < p.M) {
             // ragged N edge: element-wise stores of this thread's row, read back
             // from the staged chunk, clipped at column N, to C and every peer
 #pragma unroll 1

@@ -12,24 +12,51 @@ import paper_2108_13191_b200 as g
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _declared_functions():
-    with open(os.path.join(ROOT, "include", "gemm_f16.h")) as f:
+def _declared_functions(header="gemm_f16.h"):
+    with open(os.path.join(ROOT, "include", header)) as f:
         text = f.read()
-    return sorted(set(re.findall(r"^\s*(?:gemm_status_t|int|const char\*)\s+(\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:gemm_status_t|int|uint32_t|const char\*)\s+(\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_expected_api():
     names = _declared_functions()
     assert set(names) == set(g.EXPORTED_SYMBOLS), names
+    assert set(_declared_functions("gemm_f16_diag.h")) == set(g.DIAG_SYMBOLS)
 
 
 def test_library_loads_and_exports_every_symbol():
     lib = g.load_library()
-    for name in _declared_functions():
+    declared = _declared_functions() + _declared_functions("gemm_f16_diag.h")
+    for name in declared:
         assert hasattr(lib, name), name
     out = os.popen(f"nm -D --defined-only {g.library_path()}").read()
-    for name in _declared_functions():
+    for name in declared:
         assert re.search(rf"\bT {name}$", out, re.M), name
+
+
+def test_public_options_carry_no_diagnostic_knobs():
+    """VERDICT r01 weak #7: the product struct holds no wrong-results or rejected knobs."""
+    with open(os.path.join(ROOT, "include", "gemm_f16.h")) as f:
+        text = f.read()
+    body = text[text.index("typedef struct {"):text.index("} gemm_options_t;")]
+    fields = re.findall(r"^\s*(?:int|const void\*|void\*)\s+(\w+);", body, re.M)
+    assert fields == [f for f, _ in g._Options._fields_], fields
+    for bad in ("debug_flags", "epi_pace", "k_serpentine", "wait_hint_ns", "c_row_prefetch", "trace"):
+        assert bad not in fields
+
+
+def test_stream_k_windows_never_overlap_at_the_wrap():
+    """ADVICE r01 (medium): windows are whole and round robin, so any two launches fewer than
+    pool/window apart -- in particular the two straddling the wrap -- get disjoint windows."""
+    lib = g.load_library()
+    win = lib.gemm_f16_diag_sk_window_slots()
+    pool = lib.gemm_f16_diag_sk_pool_slots()
+    assert pool % win == 0 and win >= 16 * 74   # 16 slots per cluster, 74 clusters on a B200
+    n = pool // win
+    for start in (0, n - 3, 2 ** 32 - 5, 12345):
+        bases = [lib.gemm_f16_diag_sk_window_base((start + i) % 2 ** 32) for i in range(n)]
+        assert all(b % win == 0 and b + win <= pool for b in bases)
+        assert len(set(bases)) == n, (start, bases)
 
 
 def test_status_strings():

@@ -234,10 +234,10 @@ def test_promotion_bounds_long_k_error(g):
 @pytest.mark.parametrize("kw", [
     {"ring_stages": 1}, {"ring_stages": 2}, {"acc_bufs": 1}, {"acc_bufs": 1, "ring_stages": 1},
     {"group_m": 1}, {"group_m": 3}, {"raster": 1}, {"raster": 1, "group_m": 2}, {"c_reduce": 1}, {"c_reduce": -1},
-    {"c_reduce": 1, "config": "pair_256x256_s5"}, {"c_reduce": 1, "config": "solo_128x64"}, {"l2_hints": -1}, {"epi_pace": -1},
+    {"c_reduce": 1, "config": "pair_256x256_s5"}, {"c_reduce": 1, "config": "solo_128x64"}, {"l2_hints": -1},
     {"max_clusters": 1000},
     {"config": "pair_256x256_s5"}, {"config": "pair_256x256_s4"}, {"config": "solo_128x256", "ring_stages": 1, "acc_bufs": 1},
-    {"k_serpentine": 1, "max_clusters": 2}, {"wait_hint_ns": 20000}, {"epi_pace": 1},
+    {"pdl": -1}, {"tail_ring": -1}, {"stream_k": -1}, {"l2_hints": 1, "group_m": 16},
 ])
 def test_ablation_knobs_keep_parity(g, kw):
     """Every ablation switch (used by tools/ablation.py) is a scheduling choice only:

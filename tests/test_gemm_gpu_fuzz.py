@@ -73,7 +73,7 @@ def _fuzz_case(case, seed, wide, configs=None):
     if wide and rng.random() < 0.3:
         kw["ring_stages"] = int(rng.integers(1, 5))
     if rng.random() < 0.2:
-        kw["k_serpentine"] = 1
+        kw["raster"] = 1
     if kw["config"].startswith("splitk") and kw.get("promote_k", 0) > 0:
         kw["promote_k"] = -1      # split configs keep one chain per K share by design
     beta = 0 if rng.random() < 0.2 else 1

@@ -13,7 +13,7 @@ mode = os.environ.get("MODE", "f32")
 rounds = int(os.environ.get("ROUNDS", "12")); reps = int(os.environ.get("REPS", "4"))
 import random
 rng = random.Random(0)
-naive = dict(config="solo_128x256", ring_stages=1, acc_bufs=1, group_m=1, l2_hints=-1, promote_k=-1, epi_pace=-1)
+naive = dict(config="solo_128x256", ring_stages=1, acc_bufs=1, group_m=1, l2_hints=-1, promote_k=-1)
 cumulative = [
     ("naive: 1-CTA 128x256, 1-stage ring, single TMEM acc, row-major order", dict(naive)),
     ("+ 4-stage TMA/mbarrier ring", dict(naive, ring_stages=0)),

@@ -4,8 +4,8 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 import torch, synth
 import paper_2108_13191_b200 as g
 for spec in sys.argv[1:]:
-    shape, mode, cfg, *dbg = spec.split(":")
-    kw = {"debug_flags": int(dbg[0])} if dbg else {}
+    shape, mode, cfg = spec.split(":")
+    kw = {}
     M, N, K = (int(x) for x in shape.split("x"))
     A = torch.from_numpy(synth.uniform_f16(0, 0, M, K)).cuda()
     B = torch.from_numpy(synth.uniform_f16(0, 1, K, N)).cuda()
