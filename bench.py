@@ -9,9 +9,13 @@ FLOPs = 2MNK per GEMM (the "+C" adds are not counted).
     python bench.py [--gpus N --steps K --warmup W]       # our kernels (default)
     python bench.py --impl reference ...                   # the CPU oracle, bounded sample
 
-Multi-GPU (torchrun, one rank per GPU): batches of independent matmuls, one
-problem per GPU (BASELINE.json configs[4] "batched one-per-GPU"; weak scaling,
-no data-path collective); time = max over ranks of the device-timed region.
+Multi-GPU (torchrun, one rank per GPU), default: BASELINE.json north_star's scaling target,
+M=N=K=16384 N-sharded (configs[3]: each rank owns a column slab of B and C, A replicated, no
+communication in the GEMM phase; strong scaling).  The line reports the GEMM-phase
+efficiency T1 / (P * T_P), with T1 the unsharded problem timed on rank 0 in the same run,
+plus the NCCL all-gather of C and the fused GEMM + gather kernel (epilogue stores to every
+rank's C through symmetric memory).  `--workload batch` runs one independent problem per
+GPU instead (configs[4], weak scaling).  Time = max over ranks of the device-timed region.
 Inputs are seeded (synth/), uploaded to HBM before the timed region; the
 per-step working set (A 128 MB + B 128 MB + C 256/128 MB) exceeds the 126 MB L2.
 """
@@ -39,7 +43,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--size", type=int, default=8192, help="M = N = K")
+    ap.add_argument("--size", type=int, default=0, help="M = N = K (default 8192; 16384 for the N-shard workload)")
     ap.add_argument("--modes", default="f32,f16")
     ap.add_argument("--config", default="auto", help="kernel configuration (name in CONFIGS)")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -49,14 +53,28 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", choices=["batch", "nshard"], default="batch",
-                    help="batch: one independent n^3 problem per GPU (weak scaling, default); "
-                         "nshard: one n^3 problem N-sharded over the GPUs (strong scaling, BASELINE configs[3])")
-    ap.add_argument("--allgather", choices=["none", "nccl", "fused"], default="none",
-                    help="nshard: none; nccl = time an NCCL all-gather of the C slabs after the GEMMs; "
-                         "fused = one kernel per mode whose epilogue stores every C tile into all ranks' "
-                         "full C buffers (torch symmetric memory peers), timed as the step")
-    return ap.parse_args()
+    ap.add_argument("--workload", choices=["auto", "batch", "nshard"], default="auto",
+                    help="auto: nshard with more than one GPU, else one problem; batch: one independent n^3 "
+                         "problem per GPU (weak scaling); nshard: one n^3 problem N-sharded over the GPUs "
+                         "(strong scaling, BASELINE configs[3])")
+    ap.add_argument("--allgather", choices=["auto", "none", "nccl", "fused"], default="auto",
+                    help="nshard: auto = time both the NCCL all-gather of the C slabs and the fused "
+                         "GEMM + gather kernel (epilogue stores to all ranks' full C buffers through torch "
+                         "symmetric memory), each after the GEMM-phase region; none; nccl; fused = the "
+                         "fused kernel IS the timed step")
+    ap.add_argument("--no-t1", action="store_true", help="nshard: skip the unsharded T1 reference on rank 0")
+    ap.add_argument("--dist-backend", default="nccl",
+                    help="process-group backend (nccl; 'gloo' plus BENCH_ONE_DEVICE=1 runs every rank on cuda:0 "
+                         "-- a 1-GPU check of the multi-rank logic, never a measurement)")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.workload == "auto":
+        args.workload = "nshard" if world > 1 else "batch"
+    if args.size == 0:
+        args.size = 16384 if args.workload == "nshard" else 8192
+    if args.allgather == "auto":
+        args.allgather = "both" if (args.workload == "nshard" and world > 1) else "none"
+    return args
 
 
 def load_peaks():
@@ -243,6 +261,92 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- our arm
 
+def _time_steps(torch, dist, stream, world, dev, steps, fn):
+    """Device time (ms) of `steps` calls of fn() on `stream`, barrier + sync on both sides,
+    max over ranks."""
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def nshard_scaling(args, g, gdist, dist, torch, A, B, C, slabs, modes, M, N, K, rank, world, dev, stream, tp_ms,
+                   make_symmetric_c):
+    """SURVEY 8(e) / BASELINE north_star: GEMM-phase strong-scaling efficiency T1 / (P * T_P) at
+    the same problem, with T1 = the unsharded GEMMs timed on rank 0 in this run (the other
+    ranks idle at a barrier); then the C all-gather over NCCL and the fused GEMM + gather
+    kernel, each timed as max over ranks."""
+    out = {"P": world, "T_P_ms_per_step": tp_ms, "slab_cols": [n1 - n0 for n0, n1 in slabs]}
+    steps = max(3, min(args.steps, 10))
+    # full B and C (row-major) assembled from the slabs over NCCL: the NCCL all-gather of C
+    # is timed on the way (this IS the gather a user of the sharded GEMM would run)
+    gt = {}
+    Cfull_rm = {}
+    for m in modes:
+        gdist.allgather_c(C[m], slabs, layout="slabs")   # warm-up
+        gt[m] = _time_steps(torch, dist, stream, world, dev, steps,
+                            lambda m=m: gdist.allgather_c(C[m], slabs, layout="slabs")) / steps
+        Cfull_rm[m] = gdist.allgather_c(C[m], slabs, layout="rowmajor")
+    gbytes = {m: M * N * C[m].element_size() for m in modes}
+    out["nccl_allgather"] = {"ms_per_step": sum(gt.values()), "per_mode_ms": gt,
+                             "bytes_per_rank_received": {m: gbytes[m] * (world - 1) // world for m in modes},
+                             "busbw_gbs": {m: gbytes[m] * (world - 1) / world / (gt[m] * 1e-3) / 1e9 for m in modes},
+                             "layout": "slab-major [P][M][N/P] (all_gather_into_tensor)"}
+    out["e2e_efficiency_with_nccl_gather"] = None
+    # T1: the unsharded problem on rank 0
+    if not args.no_t1:
+        B_full = gdist.allgather_c(B, slabs, layout="rowmajor")
+        torch.cuda.synchronize()
+        t1 = None
+        if rank == 0:
+            with torch.cuda.stream(stream):
+                for m in modes:
+                    g.gemm_f16(A, B_full, Cfull_rm[m], stream=stream)
+            t1 = _time_steps(torch, dist, stream, 1, dev, steps,
+                             lambda: [g.gemm_f16(A, B_full, Cfull_rm[m], stream=stream) for m in modes]) / steps
+        dist.barrier()
+        t = torch.tensor([t1 or 0.0], device=dev, dtype=torch.float64)
+        dist.broadcast(t, 0)
+        t1 = float(t.item())
+        del B_full
+        out["T1_ms_per_step"] = t1
+        out["gemm_phase_efficiency"] = t1 / (world * tp_ms)
+        out["e2e_efficiency_with_nccl_gather"] = t1 / (world * (tp_ms + sum(gt.values())))
+        out["T1_how"] = (f"rank 0 alone, the same {M}x{N}x{K} problem unsharded ({'+'.join(modes)} per step), "
+                         f"{steps} steps after the sharded region")
+    del Cfull_rm
+    # fused GEMM + gather (one kernel per mode: epilogue TMA stores to every rank's C)
+    if args.allgather in ("both",):
+        try:
+            Cf = make_symmetric_c()
+            from paper_2108_13191_b200 import dist as gd
+
+            def fused_step():
+                for m in modes:
+                    gd.gemm_nshard_gather(A, B, Cf[m][0], slabs, rank, peer_ptrs=Cf[m][1], stream=stream)
+            with torch.cuda.stream(stream):
+                fused_step()
+            tf = _time_steps(torch, dist, stream, world, dev, steps, fused_step) / steps
+            out["fused_gemm_gather"] = {"ms_per_step": tf, "vs_gemm_only": tf / tp_ms}
+            if "T1_ms_per_step" in out:
+                out["e2e_efficiency_with_fused_gather"] = out["T1_ms_per_step"] / (world * tf)
+            del Cf
+        except Exception as ex:   # symmetric memory unavailable: report, keep the line
+            out["fused_gemm_gather"] = {"error": str(ex)[:200]}
+    return out
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
@@ -258,9 +362,17 @@ def main():
     rank, world, local = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (the product path has no CPU fallback)")
+    if os.environ.get("BENCH_ONE_DEVICE") == "1":
+        local = 0   # (logic check only: all ranks share one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 and args.dist_backend != "nccl":
+        dist.init_process_group(args.dist_backend)
+    elif world > 1:
+        # NCCL's init log (rank count, transports: NVLS / P2P over NVLink) goes to stderr, so the
+        # driver can check how many ranks the communicator really spans
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     g.load_library()
 
@@ -286,7 +398,9 @@ def main():
     C = {m: torch.from_numpy(C_h[m]).to(dev) for m in modes}
     fused = nshard and args.allgather == "fused"
     Cfull = {}
-    if fused:
+
+    def make_symmetric_c():
+        out = {}
         # every rank holds the full C (identical C_in); each step's kernel writes its
         # slab into all ranks' buffers (peer pointers from symmetric memory)
         for m in modes:
@@ -296,10 +410,14 @@ def main():
                 t.copy_(torch.from_numpy(full_h))
             else:
                 t, peers, hdl = torch.from_numpy(full_h).to(dev), [], None
-            Cfull[m] = (t, peers, hdl)
+            out[m] = (t, peers, hdl)
         if world > 1:
             torch.cuda.synchronize()
             dist.barrier()
+        return out
+
+    if fused:
+        Cfull = make_symmetric_c()
     stream = torch.cuda.Stream(dev)
     flops = 2.0 * M * nr * K          # this rank's FLOPs per GEMM
     job_flops = 2.0 * M * N * K * (1 if nshard else world)   # whole job, per GEMM mode
@@ -466,22 +584,10 @@ def main():
         gather = {"mode": "fused", "ms_per_step": None,
                   "bytes_gathered_per_step": sum(M * N * Cfull[m][0].element_size() for m in modes),
                   "note": "the gather is inside the timed GEMM kernels (epilogue TMA stores to all ranks' C)"}
-    if nshard and args.allgather == "nccl" and world > 1:
-        g0 = torch.cuda.Event(enable_timing=True)
-        g1 = torch.cuda.Event(enable_timing=True)
-        gdist.allgather_c(C[modes[0]], slabs, layout="slabs")
-        torch.cuda.synchronize()
-        dist.barrier()
-        g0.record()
-        for m in modes:
-            gdist.allgather_c(C[m], slabs, layout="slabs")
-        g1.record()
-        torch.cuda.synchronize()
-        gms = torch.tensor([g0.elapsed_time(g1)], device=dev, dtype=torch.float64)
-        dist.all_reduce(gms, op=dist.ReduceOp.MAX)
-        gbytes = sum(M * N * C[m].element_size() for m in modes)
-        gather = {"mode": "nccl", "ms_per_step": float(gms.item()), "bytes_gathered_per_step": gbytes,
-                  "e2e_tflops_with_gather": job_flops * len(modes) / ((elapsed_ms / args.steps + float(gms.item())) * 1e-3) / 1e12}
+    scaling_block = None
+    if nshard and world > 1:
+        scaling_block = nshard_scaling(args, g, gdist, dist, torch, A, B, C, slabs, modes, M, N, K, rank, world, dev,
+                                       stream, elapsed_ms / args.steps, make_symmetric_c)
 
     # --------------------------------------------------------- sampled parity of this launch config
     parity = None
@@ -547,6 +653,10 @@ def main():
                                 "sw_power_cap shows up in the longer 'sustained' window)"),
             "parity": parity,
             "allgather": gather,
+            "nshard_scaling": scaling_block,
+            "comm": ({"backend": dist.get_backend(), "nranks": dist.get_world_size(),
+                      "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version()),
+                      "init_log": "NCCL_DEBUG=INFO NCCL_DEBUG_SUBSYS=INIT on stderr"} if world > 1 else None),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

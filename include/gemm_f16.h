@@ -72,9 +72,12 @@ typedef enum {
   GEMM_CFG_PAIR_256x256_S5 = 6, /* as PAIR_256x256, 5 stages, 2 epilogue staging slots per warp */
   GEMM_CFG_PAIR_256x256_S4 = 7, /* as PAIR_256x256, 4 stages, 3 epilogue staging slots per warp */
   GEMM_CFG_PAIR_256x256_K128 = 8, /* as PAIR_256x256 with 128-deep K stages (3 stages)        */
-  GEMM_CFG_PAIR_256x512 = 9, /* GEMM_ACC_F16 only: cta_group::2, 2 UMMAs 256x256x16 per K step
-                                (256 x 512 pair tile), one TMEM chain over all of K, C_in held
-                                in registers; GEMM_ERR_INVALID_VALUE with GEMM_ACC_F32 */
+  GEMM_CFG_PAIR_256x512 = 9, /* cta_group::2, 2 UMMAs 256x256x16 per K step (256 x 512 pair
+                                tile).  F16 C: one TMEM chain over all of K, C_in held in
+                                registers.  F32 C: K-chunk promotion by TMA reduce-add into C
+                                at staggered points of the two accumulator halves (default
+                                promote_k 4096); N * 4 % 16 == 0 and no ReLU / accum_f16, else
+                                GEMM_ERR_INVALID_VALUE.  AUTO picks it for F16 C only */
   GEMM_CFG_SPLITK_128x256_S2 = 10, /* split-K over a 2-CTA cluster: cta_group::1 UMMA 128x256x16, each
                                       CTA one half of K, partials reduced through distributed shared
                                       memory (fixed order, no workspace); one tile per cluster.  Each
@@ -139,6 +142,15 @@ typedef struct {
                     /* staged, all output chunks are staged at once in the idle operand    */
                     /* ring and stored back to back (256x256-class pair, 1-CTA and        */
                     /* PAIR_256x512 configs)                                               */
+  int swizzle;      /* 0: default (128B swizzle everywhere); -1: ABLATION -- operands in the */
+                    /* no-swizzle UMMA layout (16-byte TMA boxes) and unswizzled epilogue   */
+                    /* staging (bank conflicts), the B200 analogue of the paper's unpadded  */
+                    /* shared memory (Sec. 3.3).  PAIR_256x256 (or AUTO) only,   */
+                    /* else GEMM_ERR_INVALID_VALUE                                         */
+  int warp_specialize; /* 0: default; -1: ABLATION -- the non-warp-specialised kernel: one  */
+                    /* 128x128 tile per CTA, one thread runs loads and MMAs as a software  */
+                    /* pipeline, the epilogue follows the mainloop (no overlap), plain     */
+                    /* global stores.  No bias / ReLU / accum_f16 (GEMM_ERR_INVALID_VALUE)  */
 } gemm_options_t;
 
 /*

@@ -69,12 +69,13 @@ class _Options(ctypes.Structure):
                 ("relu", ctypes.c_int), ("bias", ctypes.c_void_p), ("accum_f16", ctypes.c_int),
                 ("stream_k", ctypes.c_int), ("ring_stages", ctypes.c_int), ("acc_bufs", ctypes.c_int),
                 ("l2_hints", ctypes.c_int), ("pdl", ctypes.c_int), ("raster", ctypes.c_int),
-                ("c_reduce", ctypes.c_int), ("tail_ring", ctypes.c_int)]
+                ("c_reduce", ctypes.c_int), ("tail_ring", ctypes.c_int), ("swizzle", ctypes.c_int),
+                ("warp_specialize", ctypes.c_int)]
 
 
 # the option keywords of gemm_f16 that map 1:1 onto gemm_options_t ints (0 = default)
 _INT_OPTS = ("max_clusters", "group_m", "promote_k", "stream_k", "ring_stages", "acc_bufs", "l2_hints", "pdl",
-             "raster", "c_reduce", "tail_ring")
+             "raster", "c_reduce", "tail_ring", "swizzle", "warp_specialize")
 
 
 _lib = None

@@ -26,6 +26,17 @@ def stale() -> bool:
     return any(os.path.getmtime(s) > t for s in _sources())
 
 
+def build_variant(out: str, defines=()) -> str:
+    """A/B build of the same sources with extra -D flags into `out` (tools/ab_libs.py,
+    tools/ab_power.py); never the product library."""
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], os.path.join(CSRC, "gemm_api.cu"), "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB

@@ -19,7 +19,9 @@
 #include "../../include/gemm_f16_diag.h"
 #include "gemm_sm100.cuh"
 #include "gemm_sm100_wide.cuh"
+#include "gemm_sm100_wide_f32.cuh"
 #include "gemm_sm100_splitk.cuh"
+#include "gemm_sm100_nows.cuh"
 
 namespace {
 
@@ -137,12 +139,28 @@ const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
     make_splitk_desc<128, 2>(),
 };
 using CfgW16 = WCfg<4>;
+// F32 C (gemm_sm100_wide_f32.cuh): ring depth and epilogue staging slots per warp
+#ifndef G16_W32_STAGES
+#define G16_W32_STAGES 4
+#endif
+#ifndef G16_W32_SLOTS
+#define G16_W32_SLOTS 1
+#endif
+using CfgW32 = W32Cfg<G16_W32_STAGES, G16_W32_SLOTS>;
 const ConfigDesc kWideConfig{2, CfgW16::BN, CfgW16::STAGES, CfgW16::THREADS, CfgW16::BK,
-                             {0, CfgW16::SMEM_BYTES}, {0, CfgW16::CW}, {0, 128},
-                             {nullptr, &gemm_f16_sm100_wide_kernel<CfgW16, false>}};
-// the same tile with the per-element epilogue options (bias, ReLU, accum_f16) compiled in
-const KernelFn kWideExtFn = &gemm_f16_sm100_wide_kernel<CfgW16, true>;
+                             {CfgW32::SMEM_BYTES, CfgW16::SMEM_BYTES}, {CfgW32::CW, CfgW16::CW}, {128, 128},
+                             {&gemm_f16_sm100_wide_f32_kernel<CfgW32, false>, &gemm_f16_sm100_wide_kernel<CfgW16, false>}};
+// the same tiles with the per-element epilogue options compiled in: F16 C bias, ReLU,
+// accum_f16; F32 C beta = 0 and bias (F32 C with ReLU is not built: the reduce-add
+// promotion leaves no single point where the final sum is in registers)
+const KernelFn kWideExtFn[2] = {&gemm_f16_sm100_wide_f32_kernel<CfgW32, true>,
+                                &gemm_f16_sm100_wide_kernel<CfgW16, true>};
 const ConfigDesc kGatherConfig = make_desc<CfgGF32, CfgGF16>();
+// ABLATION builds (gemm_options_t.swizzle / warp_specialize = -1; never picked by AUTO)
+using CfgNsF32 = KCfg<2, 256, 6, false, 1, 64, false, 1, false>;
+using CfgNsF16 = KCfg<2, 256, 6, true, 1, 64, false, 1, false>;
+const KernelFn kNoSwizzleFn[2] = {&gemm_f16_sm100_kernel<CfgNsF32>, &gemm_f16_sm100_kernel<CfgNsF16>};
+const KernelFn kNoWsFn[2] = {&gemm_f16_sm100_nows_kernel<false>, &gemm_f16_sm100_nows_kernel<true>};
 
 const ConfigDesc& config_desc(int c) {
   if (c == GEMM_CFG_COUNT) return kGatherConfig;
@@ -153,6 +171,9 @@ const ConfigDesc& config_desc(int c) {
 // K elements accumulated in TMEM before the partial sum is promoted to F32
 // registers (R4): 2048 keeps the truncation error near 2.4e-6.
 constexpr int kDefaultPromoteK = 2048;
+// the 256 x 512 F32 kernel promotes by TMA reduce-add into C (every drain costs L2 traffic and
+// TMEM read time), with chains <= 4096 + a few k-blocks: ~5e-6 relative error, half the bar
+constexpr int kDefaultPromoteKWide32 = 4096;
 
 // ---------------------------------------------------------------- device cache
 constexpr int kMaxDevices = 64;
@@ -207,7 +228,7 @@ void init_device(int dev) {
           if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
         }
         if (c == GEMM_CFG_PAIR_256x512) {   // the option-carrying twin: same smem, same cluster
-          e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kWideExtFn),
+          e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kWideExtFn[a]),
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, cd.smem[a]);
           if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
         }
@@ -218,6 +239,14 @@ void init_device(int dev) {
         d.max_clusters[c][a] = per_sm * d.sm_count;
       }
     }
+  }
+  for (int a = 0; a < 2; ++a) {   // ablation kernels (same cluster shape as their base configs)
+    e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kNoSwizzleFn[a]), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             a ? CfgNsF16::SMEM_BYTES : CfgNsF32::SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kNoWsFn[a]), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               NwsCfg::SMEM_BYTES);
+    if (e != cudaSuccess) { d.status = GEMM_ERR_CUDA; d.cuda_error = e; return; }
   }
   void* f = nullptr;
   e = cudaGetSymbolAddress(&f, g_sk_flags);
@@ -463,6 +492,56 @@ gemm_status_t device_ready(int* dev_out) {
   return g_dev[dev].status;
 }
 
+// ABLATION: the non-warp-specialised kernel (gemm_sm100_nows.cuh), one 128 x 128 tile per CTA
+gemm_status_t launch_nows(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb,
+                          void* C, int64_t ldc, int acc_type, cudaStream_t stream, const gemm_options_t* opts,
+                          const DeviceInfo& di) {
+  (void)di;
+  if (opts->bias != nullptr || opts->relu || opts->accum_f16 || opts->max_clusters != 0 || opts->stream_k > 0)
+    return GEMM_ERR_INVALID_VALUE;
+  const int in_type = opts->in_type;
+  if (in_type != GEMM_IN_F16 && in_type != GEMM_IN_BF16) return GEMM_ERR_INVALID_VALUE;
+  const CUtensorMapDataType in_dt =
+      in_type == GEMM_IN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tm_a, tm_b;
+  if (!encode_2d(&tm_a, in_dt, 2, A, M, K, lda, 64, 128, operand_promotion(lda)) ||
+      !encode_2d(&tm_b, in_dt, 2, B, K, N, ldb, 64, 64, operand_promotion(ldb)))
+    return cuda_fail(cudaErrorInvalidValue);
+  GemmParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.M = static_cast<int>(M);
+  p.N = static_cast<int>(N);
+  p.K = static_cast<int>(K);
+  p.tiles_m = static_cast<int>(cdiv(M, 128));
+  p.tiles_n = static_cast<int>(cdiv(N, 128));
+  const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n;
+  if (tiles > 0x7fffffffLL) return GEMM_ERR_INVALID_VALUE;
+  p.num_tiles = static_cast<int>(tiles);
+  p.k_blocks = static_cast<int>(cdiv(K, 64));
+  const int promote = opts->promote_k;
+  if (promote < -1 || (promote > 0 && promote % 64 != 0)) return GEMM_ERR_INVALID_VALUE;
+  p.kb_per_chunk = promote == -1 ? p.k_blocks : (promote == 0 ? kDefaultPromoteK : promote) / 64;
+  const int rs = opts->ring_stages;
+  if (rs < 0 || rs > NwsCfg::STAGES) return GEMM_ERR_INVALID_VALUE;
+  p.ring_stages = rs == 0 ? NwsCfg::STAGES : rs;
+  p.in_bf16 = in_type == GEMM_IN_BF16;
+  p.beta0 = opts->beta0 ? 1 : 0;
+  p.c_ptr = C;
+  p.ldc = ldc;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(static_cast<unsigned>(tiles), 1, 1);
+  lc.blockDim = dim3(NwsCfg::THREADS, 1, 1);
+  lc.dynamicSmemBytes = NwsCfg::SMEM_BYTES;
+  lc.stream = stream;
+  PeerMaps pm;
+  std::memset(&pm, 0, sizeof(pm));
+  cudaError_t e = cudaLaunchKernelEx(&lc, kNoWsFn[acc_type], tm_a, tm_b, tm_a, p, pm, tm_a);
+  if (e != cudaSuccess) return cuda_fail(e);
+  t_trace = nullptr;
+  t_last_launches = 1;
+  return GEMM_OK;
+}
+
 gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb,
                      void* C, int64_t ldc, int acc_type, cudaStream_t stream, const gemm_options_t* opts,
                      void* const* peers = nullptr, int n_peers = 0) {
@@ -473,11 +552,24 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
 
   int cfg = opts ? opts->config : GEMM_CFG_AUTO;
   if (cfg < 0 || cfg >= GEMM_CFG_COUNT) return GEMM_ERR_INVALID_VALUE;
+  const int swz_opt = opts ? opts->swizzle : 0;
+  const int ws_opt = opts ? opts->warp_specialize : 0;
+  if (swz_opt < -1 || swz_opt > 1 || ws_opt < -1 || ws_opt > 1) return GEMM_ERR_INVALID_VALUE;
+  if (ws_opt < 0) {
+    if (n_peers > 0 || swz_opt < 0) return GEMM_ERR_INVALID_VALUE;
+    return launch_nows(M, N, K, A, lda, B, ldb, C, ldc, acc_type, stream, opts, di);
+  }
+  const bool no_swizzle = swz_opt < 0;
+  if (no_swizzle) {   // ablation build of PAIR_256x256 only
+    if ((cfg != GEMM_CFG_AUTO && cfg != GEMM_CFG_PAIR_256x256) || n_peers > 0) return GEMM_ERR_INVALID_VALUE;
+    cfg = GEMM_CFG_PAIR_256x256;
+  }
   if (cfg == GEMM_CFG_AUTO) {
     cfg = pick_config(M, N, K, acc_type, di.sm_count);
     // an explicit promote_k asks for chunked promotion, which the split-K and 256 x 512
     // kernels do not have (one chain per CTA by design): take the closest kernel that has it
-    if (opts && opts->promote_k > 0 && (config_desc(cfg).k_splits || cfg == GEMM_CFG_PAIR_256x512)) {
+    if (opts && opts->promote_k > 0 &&
+        (config_desc(cfg).k_splits || (cfg == GEMM_CFG_PAIR_256x512 && acc_type == GEMM_ACC_F16))) {
       const int64_t pair_tiles = cdiv(M, 256) * cdiv(N, 256);
       cfg = (M <= 128 || 2 * pair_tiles <= di.sm_count / 2) ? GEMM_CFG_SOLO_128x64
             : (opts->promote_k % 128 == 0 ? GEMM_CFG_PAIR_256x256_K128 : GEMM_CFG_PAIR_256x256);
@@ -495,14 +587,19 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   const float* bias = opts ? static_cast<const float*>(opts->bias) : nullptr;
   if (bias && !aligned16(bias)) return GEMM_ERR_MISALIGNED;
   CUtensorMap tm_a, tm_b, tm_c;
+  // (no_swizzle ablation: 16-byte-wide boxes, one column of UMMA core matrices each)
+  const CUtensorMapSwizzle op_swz = no_swizzle ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B;
+  const uint32_t op_box = no_swizzle ? 8u : 64u;
   const bool ok =
-      encode_2d(&tm_a, in_dt, 2, A, M, K, lda, 64, static_cast<uint32_t>(128 / cd.a_mc), operand_promotion(lda)) &&
-      encode_2d(&tm_b, in_dt, 2, B, K, N, ldb, 64, 64, operand_promotion(ldb)) &&
+      encode_2d(&tm_a, in_dt, 2, A, M, K, lda, op_box, static_cast<uint32_t>(128 / cd.a_mc), operand_promotion(lda),
+                op_swz) &&
+      encode_2d(&tm_b, in_dt, 2, B, K, N, ldb, op_box, 64, operand_promotion(ldb), op_swz) &&
       encode_2d(&tm_c, acc_type == GEMM_ACC_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                 acc_type == GEMM_ACC_F32 ? 4 : 2, C, M, N, ldc, static_cast<uint32_t>(cd.c_box_cols[a]),
                 cd.k_splits ? 128 : 32,   // split-K: whole 128-row boxes for the reduce-add steps
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                cd.c_row_bytes[a] == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+                no_swizzle ? CU_TENSOR_MAP_SWIZZLE_NONE
+                           : (cd.c_row_bytes[a] == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B));
   if (!ok) return cuda_fail(cudaErrorInvalidValue);
   // C_in L2-prefetch map: one box = an epilogue warp's whole region (32 rows x tile_n/2
   // columns), unswizzled -- it only drives cp.async.bulk.prefetch, never smem
@@ -540,8 +637,10 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   p.k_blocks = static_cast<int>(cdiv(K, cd.bk));
   const int promote = opts ? opts->promote_k : 0;
   if (promote < -1 || (promote > 0 && promote % cd.bk != 0)) return GEMM_ERR_INVALID_VALUE;
-  p.kb_per_chunk = promote == -1 ? p.k_blocks : (promote == 0 ? kDefaultPromoteK : promote) / cd.bk;
-  if (cfg == GEMM_CFG_PAIR_256x512 || cd.k_splits) {
+  const bool wide32 = cfg == GEMM_CFG_PAIR_256x512 && acc_type == GEMM_ACC_F32;
+  p.kb_per_chunk = promote == -1 ? p.k_blocks
+                                 : (promote == 0 ? (wide32 ? kDefaultPromoteKWide32 : kDefaultPromoteK) : promote) / cd.bk;
+  if ((cfg == GEMM_CFG_PAIR_256x512 && !wide32) || cd.k_splits) {
     if (promote > 0) return GEMM_ERR_INVALID_VALUE;   // one TMEM chain over all of K (its share) by design
     p.kb_per_chunk = std::max(p.k_blocks, 1);
   }
@@ -563,8 +662,16 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   p.bias = bias;
   p.trace = t_trace;
   const int rs = opts ? opts->ring_stages : 0;
-  if (rs < 0 || rs > cd.stages) return GEMM_ERR_INVALID_VALUE;
-  p.ring_stages = rs == 0 ? cd.stages : rs;
+  const int stages_max = wide32 ? CfgW32::STAGES : cd.stages;
+  if (rs < 0 || rs > stages_max) return GEMM_ERR_INVALID_VALUE;
+  p.ring_stages = rs == 0 ? stages_max : rs;
+  if (wide32) {
+    // reduce-add promotion: no ReLU (no point where the whole sum is in registers), no F16
+    // accumulation, N * 4 % 16 == 0 (TMA reduce-adds write whole 16-byte granules); and
+    // staggered promotion points at least ring_stages + 2 k-blocks apart (w32_bound)
+    if (p.c_ragged || p.relu || p.accum_f16 || n_peers > 0) return GEMM_ERR_INVALID_VALUE;
+    if (p.kb_per_chunk < p.k_blocks && p.kb_per_chunk / 2 < p.ring_stages + 2) return GEMM_ERR_INVALID_VALUE;
+  }
   const int ab = opts ? opts->acc_bufs : 0;
   if (ab < 0 || ab > 2) return GEMM_ERR_INVALID_VALUE;
   p.acc_bufs = ab == 0 ? 2 : ab;
@@ -617,7 +724,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   p.sk_tile0 = p.num_tiles;
   // F32 C: the two partials of a split tile meet by reduce-add (needs the reduce-add epilogue);
   // F16 C: the first part stores C_in + its partial, the second reduce-adds its own (R18)
-  const bool sk_ok = cd.sk_fn[a] != nullptr && n_peers == 0 && (a == GEMM_ACC_F16 || p.c_reduce) && !p.beta0 &&
+  const bool sk_ok = cd.sk_fn[a] != nullptr && n_peers == 0 && !no_swizzle && (a == GEMM_ACC_F16 || p.c_reduce) && !p.beta0 &&
                      p.bias == nullptr && !p.relu && !p.accum_f16 && !p.c_ragged &&
                      grid_cap * 16 <= kSkWindow &&
                      (tiles % grid_cap + grid_cap) * static_cast<int64_t>(p.k_blocks) < 0x7fffffffLL;
@@ -638,7 +745,10 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
     p.sk_flags = di.sk_flags + sk_window_base(g_dev[dev].sk_next.fetch_add(1u));
     fn = cd.sk_fn[a];
   }
-  if (cfg == GEMM_CFG_PAIR_256x512 && (p.bias != nullptr || p.relu || p.accum_f16)) fn = kWideExtFn;
+  if (cfg == GEMM_CFG_PAIR_256x512 && a == GEMM_ACC_F16 && (p.bias != nullptr || p.relu || p.accum_f16))
+    fn = kWideExtFn[a];
+  if (wide32 && (p.bias != nullptr || p.beta0)) fn = kWideExtFn[a];
+  if (no_swizzle) fn = kNoSwizzleFn[a];
   cudaError_t e = cudaLaunchKernelEx(&lc, fn, tm_a, tm_b, tm_c, p, pm, tm_cpf);
   if (e != cudaSuccess) return cuda_fail(e);
   t_trace = nullptr;   // (a trace is armed for one launch)

@@ -164,8 +164,13 @@ __device__ __forceinline__ Item item_of(const GemmParams& p, const Work& w, int 
 }
 
 template <int CG_, int BN_, int STAGES_, bool OUT_F16_, int EPI_SLOTS_ = 1, int BK_ = 64, bool PEERS_ = false,
-          int MC_ = 1>
+          int MC_ = 1, bool SW_ = true>
 struct KCfg {
+  // SW = false: ABLATION ONLY (option swizzle = -1; the B200 analogue of the paper's
+  // unpadded shared memory, Sec. 3.3): operands staged in the no-swizzle
+  // "interleaved" UMMA layout (16-byte TMA boxes, core matrices of 8 rows x 16 B) and the
+  // epilogue staging in plain rows (32 lanes of a warp hit the same banks)
+  static constexpr bool SW = SW_;
   static constexpr int CG = CG_;            // CTAs per MMA (cta_group)
   static constexpr int MC = MC_;            // cta_group::1 only: CTAs per cluster sharing (multicasting) A
   static_assert(MC == 1 || (CG == 1 && (MC == 2 || MC == 4)), "A multicast: 1-CTA tiles, 2 or 4 per cluster");
@@ -223,6 +228,18 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uin
   d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
   d |= static_cast<uint64_t>(1) << 46;
   d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+// UMMA shared-memory descriptor, no swizzle ("interleaved" canonical layout, layout type 0):
+// core matrices of 8 rows x 16 B stored contiguously; LBO / SBO are the byte strides between
+// core matrices along the leading (K for K-major, MN for MN-major) and the other dimension.
+__device__ __forceinline__ uint64_t desc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
   return d;
 }
 
@@ -326,6 +343,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   tc_fence_after();
   uint32_t tmem_base;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot) : "memory");
+  tmem_base = __shfl_sync(0xffffffffu, tmem_base, 0);   // (warp-uniform)
   // PDL: everything above (barrier init, TMEM allocation, descriptor prefetch)
   // overlapped the previous grid's tail; no global memory is touched before this
   // (bar the diagnostic trace stamps)
@@ -338,7 +356,10 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
 
   if (warp == Cfg::W_PRODUCER) {
     // ===================== TMA producer =====================
-    if (lane == 0) {
+    // The whole warp runs the loop (warp-uniform operands: no per-instruction elect/R2UR
+    // waterfall around each TMA); the elected lane issues.
+    {
+      const bool leader = elect_one();
       const uint32_t full_leader = (CG == 2) ? mapa_shared(full_bar, 0) : full_bar;
       const uint64_t pol_a = p.l2_hints ? policy_evict_last() : policy_evict_normal();
       const uint64_t pol_b = policy_evict_normal();
@@ -353,9 +374,10 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         if constexpr (MC > 1) tn = MC * tn + static_cast<int>(mrank);
         const int a_row = tm * BM * CG + static_cast<int>(rank) * BM;
         const int b_col = tn * BN + static_cast<int>(rank) * Cfg::BN_CTA;
-        if (it + 1 == work.n_items) griddep_launch_dependents();   // last tile: let the next grid ramp
+        if (it + 1 == work.n_items && leader) griddep_launch_dependents();   // last tile: let the next grid ramp
         for (int kb = itm.kb_lo; kb < itm.kb_hi; ++kb) {
           mbar_wait(empty_bar + 8 * stage, phase ^ 1u);
+          if (leader) {
           if (rank == 0) mbar_arrive_expect_tx(full_bar + 8 * stage, Cfg::STAGE_BYTES * CG);
           const uint32_t fb = full_leader + 8 * stage;
           const uint32_t a_dst = sA + stage * Cfg::A_BYTES;
@@ -363,7 +385,16 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
 #pragma unroll
           for (int kh = 0; kh < Cfg::KH; ++kh) {
             const int kc = kb * BK + 64 * kh;
-            if constexpr (CG == 2) {
+            if constexpr (CG == 2 && !Cfg::SW) {
+              // no swizzle: 16-byte-wide boxes -- A: 8 K-columns x 128 rows (2 KB), B: 8 N-columns
+              // x 64 K-rows (1 KB), each one column of core matrices
+#pragma unroll
+              for (int g = 0; g < 8; ++g)
+                tma_load_2d_pair_hint(a_dst + kh * Cfg::A_HALF_BYTES + g * 2048, &tm_a, kc + 8 * g, a_row, fb, pol_a);
+#pragma unroll
+              for (int g = 0; g < Cfg::BN_CTA / 8; ++g)
+                tma_load_2d_pair_hint(b_dst + kh * Cfg::B_HALF_BYTES + g * 1024, &tm_b, b_col + 8 * g, kc, fb, pol_b);
+            } else if constexpr (CG == 2) {
               tma_load_2d_pair_hint(a_dst + kh * Cfg::A_HALF_BYTES, &tm_a, kc, a_row, fb, pol_a);
 #pragma unroll
               for (int h = 0; h < Cfg::BN_CTA / 64; ++h)
@@ -385,13 +416,17 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                                  fb, pol_b);
             }
           }
+          }   // leader
+          __syncwarp();
           if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
         }
       }
     }
   } else if (warp == Cfg::W_MMA) {
     // ===================== MMA issuer (pair leader) =====================
-    if (rank == 0 && lane == 0) {
+    // the whole warp runs the loop (uniform control flow and operands); the elected lane issues
+    if (rank == 0) {
+      const bool leader = elect_one();
       const uint32_t idesc = (idesc_f16_f32acc<BM * CG, BN>() & (p.accum_f16 ? ~(3u << 4) : ~0u)) |
                              (p.in_bf16 ? ((1u << 7) | (1u << 10)) : 0u);
       int stage = 0;
@@ -402,7 +437,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       for (; it < work.n_items; ++it) {
         const Item itm = item_of<SK>(p, work, cluster, nclusters, it);
         const int n_chunks = SK ? (itm.kb_hi - itm.kb_lo + p.kb_per_chunk - 1) / p.kb_per_chunk : p.k_chunks;
-        const bool tr = trace_me && it < 60;
+        const bool tr = trace_me && leader && it < 60;
         uint64_t clk0 = 0;
         if (tr) {
           p.trace[8 * it + 0] = globaltimer_ns();
@@ -423,20 +458,32 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
 #pragma unroll
             for (int k = 0; k < BK / Cfg::UMMA_K; ++k) {
               // A (K-major): advance 16 elements = 32 B inside the 128B swizzle row.
-              const uint64_t adesc = desc_sw128(a_s + (k >> 2) * Cfg::A_HALF_BYTES + 32 * (k & 3), 16, 1024);
-              // B (MN-major): advance 16 k-rows = 2 swizzle atoms of 8 rows x 128 B;
-              // 64-column groups are B_ATOM_BYTES apart (LBO), 8-row groups 1 KB (SBO).
-              const uint64_t bdesc = desc_sw128(b_s + (k >> 2) * Cfg::B_HALF_BYTES + 2048 * (k & 3),
-                                                Cfg::B_ATOM_BYTES, 1024);
-              umma_f16<CG>(d_tmem, adesc, bdesc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              uint64_t adesc, bdesc;
+              if constexpr (Cfg::SW) {
+                adesc = desc_sw128(a_s + (k >> 2) * Cfg::A_HALF_BYTES + 32 * (k & 3), 16, 1024);
+                // B (MN-major): advance 16 k-rows = 2 swizzle atoms of 8 rows x 128 B;
+                // 64-column groups are B_ATOM_BYTES apart (LBO), 8-row groups 1 KB (SBO).
+                bdesc = desc_sw128(b_s + (k >> 2) * Cfg::B_HALF_BYTES + 2048 * (k & 3), Cfg::B_ATOM_BYTES, 1024);
+              } else {
+                // A: K-direction core matrices are the 2 KB boxes (LBO), 8-row groups 128 B (SBO);
+                // a K=16 step spans two boxes.  B: N-direction core matrices 1 KB apart (LBO),
+                // 8-k-row groups 128 B (SBO); a K=16 step spans two of those.
+                adesc = desc_noswz(a_s + (k >> 2) * Cfg::A_HALF_BYTES + 4096 * (k & 3), 2048, 128);
+                bdesc = desc_noswz(b_s + (k >> 2) * Cfg::B_HALF_BYTES + 256 * (k & 3), 1024, 128);
+              }
+              if (leader) umma_f16<CG>(d_tmem, adesc, bdesc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             }
-            if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, 0x3);
-            else if constexpr (MC > 1) umma_commit_mc(empty_bar + 8 * stage, (1u << MC) - 1u);   // every CTA's stage
-            else umma_commit(empty_bar + 8 * stage);
+            if (leader) {
+              if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, 0x3);
+              else if constexpr (MC > 1) umma_commit_mc(empty_bar + 8 * stage, (1u << MC) - 1u);   // every CTA's stage
+              else umma_commit(empty_bar + 8 * stage);
+            }
             if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
           }
-          if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, 0x3);
-          else umma_commit(accf_bar + 8 * acc);
+          if (leader) {
+            if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, 0x3);
+            else umma_commit(accf_bar + 8 * acc);
+          }
           if (tr && ch == n_chunks - 1) {
             p.trace[8 * it + 2] = globaltimer_ns();
             p.trace[8 * it + 7] = clock64() - clk0;   // SM cycles of this tile (MMA warp)
@@ -562,7 +609,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         }
 #pragma unroll
         for (int j = 0; j < Cfg::RB / 16; ++j) {
-          const uint32_t addr = sbuf + swz<Cfg::RB>(lane, static_cast<uint32_t>(j));
+          const uint32_t addr = sbuf + (Cfg::SW ? swz<Cfg::RB>(lane, static_cast<uint32_t>(j)) : lane * Cfg::RB + 16u * static_cast<uint32_t>(j));
           const float* a = &racc[c * Cfg::CW + j * (16 / Cfg::ESIZE)];
           constexpr int EPU = 16 / Cfg::ESIZE;      // output elements per 16-byte unit
           float o[EPU];
@@ -631,7 +678,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
             // from the staged chunk, clipped at column N, to C and every peer
 #pragma unroll 1
             for (int j = 0; j < Cfg::RB / 16; ++j) {
-              const uint4 v = lds128u(sbuf + swz<Cfg::RB>(lane, static_cast<uint32_t>(j)));
+              const uint4 v = lds128u(sbuf + (Cfg::SW ? swz<Cfg::RB>(lane, static_cast<uint32_t>(j)) : lane * Cfg::RB + 16u * static_cast<uint32_t>(j)));
               const uint32_t o[4] = {v.x, v.y, v.z, v.w};
               constexpr int EPU = 16 / Cfg::ESIZE;   // elements per 16-byte unit
               const int cb = ccol + EPU * j;

@@ -145,15 +145,18 @@ gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
   tc_fence_after();
   uint32_t tmem_base;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot) : "memory");
+  tmem_base = __shfl_sync(0xffffffffu, tmem_base, 0);   // (warp-uniform)
   griddep_wait();
   if (tr) p.trace[1] = globaltimer_ns();
 
   if (warp == Cfg::W_PRODUCER) {
     // ===================== TMA producer: this CTA's share of K =====================
-    if (lane == 0) {
-      griddep_launch_dependents();
+    // (the whole warp runs the loop: warp-uniform TMA operands; the elected lane issues)
+    {
+      const bool leader = elect_one();
+      if (leader) griddep_launch_dependents();
       if constexpr (Cfg::DMA) {
-        if (load_c) {   // C_in slice now (its own region), ready long before the reduction
+        if (load_c && leader) {   // C_in slice now (its own region), ready long before the reduction
           mbar_arrive_expect_tx(cin_bar, Cfg::CIN_BYTES);
           tma_load_2d_hint(base + Cfg::OFF_CIN_DMA, &tm_cin, tn * BN + static_cast<int>(r) * CW, tm * BM, cin_bar,
                            policy_evict_first());
@@ -164,19 +167,24 @@ gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
       uint32_t phase = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(empty_bar + 8 * stage, phase ^ 1u);
-        mbar_arrive_expect_tx(full_bar + 8 * stage, Cfg::STAGE_BYTES);
         const int kc = kb * BK;
-        tma_load_2d_hint(sA + stage * Cfg::A_BYTES, &tm_a, kc, tm * BM, full_bar + 8 * stage, pol);
+        if (leader) {
+          mbar_arrive_expect_tx(full_bar + 8 * stage, Cfg::STAGE_BYTES);
+          tma_load_2d_hint(sA + stage * Cfg::A_BYTES, &tm_a, kc, tm * BM, full_bar + 8 * stage, pol);
 #pragma unroll
-        for (int h = 0; h < BN / 64; ++h)
-          tma_load_2d_hint(sB + stage * Cfg::B_BYTES + h * Cfg::B_ATOM_BYTES, &tm_b, tn * BN + 64 * h, kc,
-                           full_bar + 8 * stage, pol);
+          for (int h = 0; h < BN / 64; ++h)
+            tma_load_2d_hint(sB + stage * Cfg::B_BYTES + h * Cfg::B_ATOM_BYTES, &tm_b, tn * BN + 64 * h, kc,
+                             full_bar + 8 * stage, pol);
+        }
+        __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1u; }
       }
     }
   } else if (warp == Cfg::W_MMA) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
+    // (the whole warp runs the loop: uniform operands; the elected lane issues)
+    {
+      const bool leader = elect_one();
       const uint32_t idesc = (idesc_f16_f32acc<BM, BN>() & (p.accum_f16 ? ~(3u << 4) : ~0u)) |
                              (p.in_bf16 ? ((1u << 7) | (1u << 10)) : 0u);
       int stage = 0;
@@ -188,12 +196,13 @@ gemm_f16_sm100_splitk_kernel(const __grid_constant__ CUtensorMap tm_a,
         const uint32_t b_s = sB + stage * Cfg::B_BYTES;
 #pragma unroll
         for (int k = 0; k < BK / Cfg::UMMA_K; ++k)
-          umma_f16<1>(tmem_base, desc_sw128(a_s + 32 * k, 16, 1024),
-                      desc_sw128(b_s + 2048 * k, Cfg::B_ATOM_BYTES, 1024), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-        umma_commit(empty_bar + 8 * stage);
+          if (leader)
+            umma_f16<1>(tmem_base, desc_sw128(a_s + 32 * k, 16, 1024),
+                        desc_sw128(b_s + 2048 * k, Cfg::B_ATOM_BYTES, 1024), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+        if (leader) umma_commit(empty_bar + 8 * stage);
         if (++stage == STAGES) { stage = 0; phase ^= 1u; }
       }
-      umma_commit(accf_bar);   // with no k-blocks (K split finer than K) it arrives at once
+      if (leader) umma_commit(accf_bar);   // with no k-blocks (K split finer than K) it arrives at once
     }
   } else {
     mbar_wait(accf_bar, 0);    // this CTA's accumulator is complete (and its ring idle)

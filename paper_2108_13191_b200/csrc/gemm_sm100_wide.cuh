@@ -127,6 +127,7 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
   tc_fence_after();
   uint32_t tmem_base;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot) : "memory");
+  tmem_base = __shfl_sync(0xffffffffu, tmem_base, 0);   // (warp-uniform)
   griddep_wait();   // PDL: nothing above touched global memory
 
   const int cluster = static_cast<int>(blockIdx.x) / 2;
@@ -134,7 +135,9 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
 
   if (warp == Cfg::W_PRODUCER) {
     // ===================== TMA producer =====================
-    if (lane == 0) {
+    // (the whole warp runs the loop: warp-uniform TMA operands; the elected lane issues)
+    {
+      const bool leader = elect_one();
       const uint32_t full_leader = mapa_shared(full_bar, 0);
       const uint64_t pol_a = p.l2_hints ? policy_evict_last() : policy_evict_normal();
       const uint64_t pol_b = policy_evict_normal();
@@ -146,9 +149,10 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
         const int a_row = tm * BM * 2 + static_cast<int>(rank) * BM;
         // UMMA h covers columns [512 tn + 256 h, +256); CTA r stages its 128-column half
         const int b_col = tn * Cfg::BN + static_cast<int>(rank) * 128;
-        if (tile + nclusters >= p.num_tiles) griddep_launch_dependents();
+        if (tile + nclusters >= p.num_tiles && leader) griddep_launch_dependents();
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(empty_bar + 8 * stage, phase ^ 1u);
+          if (leader) {
           if (rank == 0) mbar_arrive_expect_tx(full_bar + 8 * stage, Cfg::STAGE_BYTES * 2);
           const uint32_t fb = full_leader + 8 * stage;
           const uint32_t a_dst = sA + stage * Cfg::A_BYTES;
@@ -161,13 +165,17 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
             for (int t = 0; t < 2; ++t)
               tma_load_2d_pair_hint(b_dst + h * Cfg::B_HALF_BYTES + t * Cfg::B_ATOM_BYTES, &tm_b,
                                     b_col + h * Cfg::UMMA_N + 64 * t, kc, fb, pol_b);
+          }   // leader
+          __syncwarp();
           if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
         }
       }
     }
   } else if (warp == Cfg::W_MMA) {
     // ===================== MMA issuer (pair leader) =====================
-    if (rank == 0 && lane == 0) {
+    // the whole warp runs the loop (uniform control flow and operands); the elected lane issues
+    if (rank == 0) {
+      const bool leader = elect_one();
       const uint32_t idesc = (idesc_f16_f32acc<256, 256>() & (p.accum_f16 ? ~(3u << 4) : ~0u)) |
                              (p.in_bf16 ? ((1u << 7) | (1u << 10)) : 0u);
       // the 4 K=16 UMMAs of one k-block for accumulator half h
@@ -176,7 +184,7 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
         const uint32_t b_s = sB + stage * Cfg::B_BYTES + h * Cfg::B_HALF_BYTES;
 #pragma unroll
         for (int k = 0; k < BK / Cfg::UMMA_K; ++k)
-          umma_f16<2>(tmem_base + static_cast<uint32_t>(h * Cfg::UMMA_N), desc_sw128(a_s + 32 * k, 16, 1024),
+          if (leader) umma_f16<2>(tmem_base + static_cast<uint32_t>(h * Cfg::UMMA_N), desc_sw128(a_s + 32 * k, 16, 1024),
                       desc_sw128(b_s + 2048 * k, Cfg::B_ATOM_BYTES, 1024), idesc, (first && k == 0) ? 0u : 1u);
       };
       // split k-blocks per tile end: ring_stages - 1 leaves one stage for the next tile's
@@ -187,7 +195,7 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
       uint32_t acc_phase = 0;
       int it = 0;
       for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
-        const bool tr = p.trace != nullptr && blockIdx.x == 0 && it < 60;
+        const bool tr = p.trace != nullptr && blockIdx.x == 0 && leader && it < 60;
         uint64_t clk0 = 0;
         if (tr) {
           p.trace[8 * it + 0] = globaltimer_ns();
@@ -208,15 +216,15 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
             mma_half(s, 0, i == 0);
             if (++s == p.ring_stages) { s = 0; ph ^= 1u; }
           }
-          if (tail == 0) umma_commit_pair(accf_bar, 0x3);
+          if (tail == 0 && leader) umma_commit_pair(accf_bar, 0x3);
           mbar_wait(acce_bar + 8, acc_phase ^ 1u);
           tc_fence_after();
           for (int i = 0; i < head; ++i) {
             mma_half(stage, 1, i == 0);
-            umma_commit_pair(empty_bar + 8 * stage, 0x3);
+            if (leader) umma_commit_pair(empty_bar + 8 * stage, 0x3);
             if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
           }
-          if (tail == 0) umma_commit_pair(accf_bar + 8, 0x3);
+          if (tail == 0 && leader) umma_commit_pair(accf_bar + 8, 0x3);
         }
         // ---- middle: both halves per k-block
         for (int kb = head; kb < p.k_blocks - tail; ++kb) {
@@ -224,7 +232,7 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
           tc_fence_after();
           mma_half(stage, 0, false);
           mma_half(stage, 1, false);
-          umma_commit_pair(empty_bar + 8 * stage, 0x3);
+          if (leader) umma_commit_pair(empty_bar + 8 * stage, 0x3);
           if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
         }
         // ---- tail: all h0 MMAs, hand h0 to the epilogue, then the h1 MMAs
@@ -237,13 +245,13 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
             mma_half(s, 0, false);
             if (++s == p.ring_stages) { s = 0; ph ^= 1u; }
           }
-          umma_commit_pair(accf_bar, 0x3);
+          if (leader) umma_commit_pair(accf_bar, 0x3);
           for (int i = 0; i < tail; ++i) {
             mma_half(stage, 1, false);
-            umma_commit_pair(empty_bar + 8 * stage, 0x3);
+            if (leader) umma_commit_pair(empty_bar + 8 * stage, 0x3);
             if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
           }
-          umma_commit_pair(accf_bar + 8, 0x3);
+          if (leader) umma_commit_pair(accf_bar + 8, 0x3);
         }
         if (tr) {
           p.trace[8 * it + 2] = globaltimer_ns();

@@ -238,6 +238,8 @@ def test_promotion_bounds_long_k_error(g):
     {"max_clusters": 1000},
     {"config": "pair_256x256_s5"}, {"config": "pair_256x256_s4"}, {"config": "solo_128x256", "ring_stages": 1, "acc_bufs": 1},
     {"pdl": -1}, {"tail_ring": -1}, {"stream_k": -1}, {"l2_hints": 1, "group_m": 16},
+    {"swizzle": -1}, {"swizzle": -1, "ring_stages": 1}, {"swizzle": -1, "promote_k": 256},
+    {"warp_specialize": -1}, {"warp_specialize": -1, "ring_stages": 1}, {"warp_specialize": -1, "promote_k": 512},
 ])
 def test_ablation_knobs_keep_parity(g, kw):
     """Every ablation switch (used by tools/ablation.py) is a scheduling choice only:

@@ -11,7 +11,8 @@ must equal the oracle's C_round (RNE of the exact double result) exactly.
 
 Output paths (the kernels and epilogue variants that write C):
   f32: staged C_in (c_reduce off), TMA reduce-add (default), 1-CTA, split-K
-       (reduce-add steps), stream-K (token-ordered reduce-adds)
+       (reduce-add steps), stream-K (token-ordered reduce-adds), 256x512 wide tile
+       (K-chunk promotion by reduce-adds at staggered points)
   f16: pair tile (C_in staged in smem), 256x512 wide tile (C_in held in registers),
        1-CTA, split-K (DSMEM exchange), stream-K (R18: store + F16 reduce-add)
 """
@@ -33,6 +34,7 @@ PATHS = [
     ("f32_splitk_s2", "f32", dict(config="splitk_128x128_s2")),
     ("f32_splitk_s4", "f32", dict(config="splitk_128x256_s4")),
     ("f32_streamk", "f32", dict(config="pair_256x256_k128", stream_k=1, max_clusters=4)),
+    ("f32_wide", "f32", dict(config="pair_256x512", promote_k=768)),
     ("f16_pair", "f16", dict(config="pair_256x256_k128")),
     ("f16_pair_s5", "f16", dict(config="pair_256x256_s5")),
     ("f16_wide", "f16", dict(config="pair_256x512")),

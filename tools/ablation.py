@@ -35,6 +35,11 @@ removals = [
     ("full - raster (row-major tiles)", dict(group_m=1)),
     ("full - L2 hints", dict(l2_hints=-1)),
     ("full - promotion", dict(promote_k=-1)),
+    ("full - 128-deep stages - swizzle (no-swizzle UMMA layout, 16-byte TMA boxes, unswizzled epilogue staging)",
+     dict(config="pair_256x256", swizzle=-1)),
+    ("full - warp specialisation (1 thread pipelines TMA + MMA, 128x128 per CTA, epilogue after the mainloop)",
+     dict(warp_specialize=-1)),
+    ("full - warp specialisation, 1-stage pipeline (the paper's single stage)", dict(warp_specialize=-1, ring_stages=1)),
 ]
 variants = cumulative + removals
 A = torch.from_numpy(synth.uniform_f16(0, 0, n, n)).cuda()

@@ -16,6 +16,10 @@ KEYS = {
     "launch__cluster_size": "cluster",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum": "smem_bank_conflicts_ld",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum": "smem_bank_conflicts_st",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum": "smem_st_wavefronts",
+    "smsp__sass_inst_executed_op_shared_st.sum": "smem_st_instructions",
 }
 
 

@@ -12,6 +12,8 @@ C = torch.from_numpy((synth.uniform_f32 if mode == "f32" else synth.uniform_f16)
 tr = torch.zeros(512, dtype=torch.int64, device="cuda")
 CTA = int(os.environ.get("TRACE_CTA", "0"))   # CTA to trace (rank 0 of a pair: even)
 tr[8 * 63 + 7] = CTA
+if os.environ.get("TRACE_LIB"):   # trace another build of the library (same ABI)
+    g._build.LIB = os.path.abspath(os.environ["TRACE_LIB"]); g._lib = None; g.load_library(build_if_missing=False)
 for _ in range(5): g.gemm_f16(A, B, C, **kw)
 g.gemm_f16(A, B, C, trace=tr, **kw)
 torch.cuda.synchronize()
