@@ -232,8 +232,10 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uin
 }
 
 // UMMA shared-memory descriptor, no swizzle ("interleaved" canonical layout, layout type 0):
-// core matrices of 8 rows x 16 B stored contiguously; LBO / SBO are the byte strides between
-// core matrices along the leading (K for K-major, MN for MN-major) and the other dimension.
+// core matrices of 8 rows x 16 B stored contiguously.  For both majors LBO is the byte stride
+// between core matrices adjacent along K and SBO the stride between those adjacent along M / N
+// (cute's make_umma_desc for SWIZZLE_NONE: K-major ((8,m),(T,2)):((1T,SBO),(1,LBO)), MN-major
+// ((1,n),(8,k)):((X,SBO),(1,LBO)) in 16-byte units).
 __device__ __forceinline__ uint64_t desc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
@@ -465,11 +467,12 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                 // 64-column groups are B_ATOM_BYTES apart (LBO), 8-row groups 1 KB (SBO).
                 bdesc = desc_sw128(b_s + (k >> 2) * Cfg::B_HALF_BYTES + 2048 * (k & 3), Cfg::B_ATOM_BYTES, 1024);
               } else {
-                // A: K-direction core matrices are the 2 KB boxes (LBO), 8-row groups 128 B (SBO);
-                // a K=16 step spans two boxes.  B: N-direction core matrices 1 KB apart (LBO),
-                // 8-k-row groups 128 B (SBO); a K=16 step spans two of those.
+                // K-major A: LBO = K-direction core-matrix stride (the 2 KB boxes), SBO = 8-row
+                // groups (128 B); a K=16 step spans two boxes.  MN-major B: LBO = K-direction
+                // stride (8-k-row groups, 128 B), SBO = N-direction core matrices (the 1 KB
+                // boxes); a K=16 step spans two 8-k-row groups.
                 adesc = desc_noswz(a_s + (k >> 2) * Cfg::A_HALF_BYTES + 4096 * (k & 3), 2048, 128);
-                bdesc = desc_noswz(b_s + (k >> 2) * Cfg::B_HALF_BYTES + 256 * (k & 3), 1024, 128);
+                bdesc = desc_noswz(b_s + (k >> 2) * Cfg::B_HALF_BYTES + 256 * (k & 3), 128, 1024);
               }
               if (leader) umma_f16<CG>(d_tmem, adesc, bdesc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             }
