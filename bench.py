@@ -53,6 +53,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-small", action="store_true", help="skip the configs[0]/configs[1] small-shape record")
     ap.add_argument("--workload", choices=["auto", "batch", "nshard"], default="auto",
                     help="auto: nshard with more than one GPU, else one problem; batch: one independent n^3 "
                          "problem per GPU (weak scaling); nshard: one n^3 problem N-sharded over the GPUs "
@@ -347,6 +348,54 @@ def nshard_scaling(args, g, gdist, dist, torch, A, B, C, slabs, modes, M, N, K, 
     return out
 
 
+SMALL_SHAPES = (("configs[0]", 256, "f32"), ("configs[1]", 1024, "f16"))
+
+
+def small_shapes(g, torch, synth, dev, peaks, reps=20, rounds=5):
+    """BASELINE.json configs[0] (256^3 F32 acc) and configs[1] (1024^3 F16 acc): GPU time
+    per GEMM from CUDA-graph replay (`reps` launches captured in one graph, median over
+    `rounds` replays, CUDA events on the replay stream), so the host enqueue cost of a
+    call (~7-11 us) is not counted; against the roofline time of the shape,
+    max(2MNK / tensor peak, compulsory bytes / HBM peak), compulsory bytes =
+    2(MK + KN) + 2 MN sizeof(C) (C_in read + C_out written).  Inputs fit in L2 here, so
+    the HBM term is a floor the kernel need not pay (frac can exceed 1 in principle)."""
+    out = {}
+    s = torch.cuda.Stream(dev)
+    for name, n, mode in SMALL_SHAPES:
+        A = torch.from_numpy(synth.uniform_f16(0, synth.MATRIX_A, n, n)).to(dev)
+        B = torch.from_numpy(synth.uniform_f16(0, synth.MATRIX_B, n, n)).to(dev)
+        C = torch.from_numpy((synth.uniform_f32 if mode == "f32" else synth.uniform_f16)(0, synth.MATRIX_C, n, n)).to(dev)
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                g.gemm_f16(A, B, C, stream=s)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            for _ in range(reps):
+                g.gemm_f16(A, B, C, stream=s)
+        graph.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(rounds):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            graph.replay()
+            e1.record(s)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / reps * 1e3)
+        us = statistics.median(ts)
+        flops = 2.0 * n ** 3
+        byts = 2 * (2 * n * n) + 2 * n * n * (4 if mode == "f32" else 2)
+        t_tc = flops / (peaks["tflops"] * 1e12) * 1e6
+        t_hbm = byts / (peaks["hbm_gbs"] * 1e9) * 1e6
+        out[name] = {"M": n, "N": n, "K": n, "mode": mode, "us": round(us, 3), "tflops": round(flops / us / 1e6, 2),
+                     "roofline_us": round(max(t_tc, t_hbm), 3), "bound": "hbm" if t_hbm > t_tc else "tensor",
+                     "frac": round(max(t_tc, t_hbm) / us, 4), "config": g.pick_config(n, n, n, 0 if mode == "f32" else 1),
+                     "how": f"{reps} launches in one CUDA graph, median of {rounds} replays"}
+        del graph
+    return out
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
@@ -612,6 +661,10 @@ def main():
                 ok &= rel <= 2e-3
         parity["pass"] = bool(ok)
 
+    small = None
+    if rank == 0 and not args.no_small:
+        small = small_shapes(g, torch, synth, dev, load_peaks())
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_sample_rate(n, modes, args.cpu_seconds)
@@ -652,6 +705,7 @@ def main():
                                 "burst region and before the sustained window (power-capped, "
                                 "sw_power_cap shows up in the longer 'sustained' window)"),
             "parity": parity,
+            "small_shapes": small,
             "allgather": gather,
             "nshard_scaling": scaling_block,
             "comm": ({"backend": dist.get_backend(), "nranks": dist.get_world_size(),
