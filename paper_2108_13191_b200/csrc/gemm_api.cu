@@ -402,14 +402,18 @@ int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
     const int64_t sm4 = sm_count - sm_count / 9;
     const bool f32 = acc_type == GEMM_ACC_F32;
     if (K >= 2048 && 4 * t128 <= sm4 && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x128_S4;
-    // F32 reduces by TMA reduce-add: S4 x 128x256 from K = 4096, S2 x 128x128 from K = 1024,
-    // S2 x 128x256 from K = 2048.  F16 exchanges through DSMEM, where the bulk-DMA configs
-    // (S2 x 128x128, S2 x 128x256) beat the pushes of S4 x 128x256 until K = 16384
-    // (splitk.md v9/v10)
-    if (f32 && K >= 4096 && 4 * t256 <= sm4 && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S4;
+    // F32 reduces by TMA reduce-add, F16 through DSMEM (bulk-DMA configs S2 x 128x128 and
+    // S2 x 128x256 beat the pushes of S4 x 128x256 until K = 16384, splitk.md v9/v10).
+    // The two-way splits pay only from K = 4096 in either mode, the four-way 128x256 split
+    // for F32 from K = 8192: below that the 1-CTA tiles win (graph replay, round 2:
+    // 1024^2 x 1024 F32 6.4 vs 7.9 us, 1024^2 x 2048 F16 8.8 vs 10.8 us, 768^2 x 4096 F32
+    // S2 x 128x128 11.5 vs S4 x 128x256 14.7 us; profiles/r02/graph_small_pick*.jsonl).
+    // S2 x 128x256 is not picked: wherever its 2 * t256 CTAs fit one wave the 1-CTA
+    // 128 x 128 tiles do too, and win (1024 x 2048 x 4096: 17.7 vs 19.2 us F32, 17.4 vs
+    // 21.8 us F16)
+    if (f32 && K >= 8192 && 4 * t256 <= sm4 && K <= 4 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S4;
     if (!f32 && K >= 16384 && 4 * t256 <= sm4) return GEMM_CFG_SPLITK_128x256_S4;
-    if (K >= (f32 ? 1024 : 2048) && 2 * t128 <= sm_count && K <= 2 * kmax_chain) return GEMM_CFG_SPLITK_128x128_S2;
-    if (K >= (f32 ? 2048 : 4096) && 2 * t256 <= sm_count && K <= 2 * kmax_chain) return GEMM_CFG_SPLITK_128x256_S2;
+    if (K >= 4096 && 2 * t128 <= sm_count && K <= 2 * kmax_chain) return GEMM_CFG_SPLITK_128x128_S2;
     if (small) {
       if (M <= 128) return cdiv(N, 256) >= sm_count ? GEMM_CFG_SOLO_128x256 : GEMM_CFG_SOLO_128x64;
       return GEMM_CFG_SOLO_128x64;

@@ -37,6 +37,11 @@
 #include <cuda.h>
 #include "ptx.cuh"
 
+#ifndef G16_DIAG_NO_MMA
+#define G16_DIAG_NO_MMA 0   // DIAGNOSTIC builds only (wrong results): 1 = the MMA warp skips the
+                            // tcgen05.mma instructions, so the TMA ring runs alone
+#endif
+
 namespace g16 {
 
 // Extra destinations of the C tile (fused N-shard all-gather, gemm_f16_gather):
@@ -474,7 +479,9 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                 adesc = desc_noswz(a_s + (k >> 2) * Cfg::A_HALF_BYTES + 4096 * (k & 3), 2048, 128);
                 bdesc = desc_noswz(b_s + (k >> 2) * Cfg::B_HALF_BYTES + 256 * (k & 3), 128, 1024);
               }
+#if !G16_DIAG_NO_MMA
               if (leader) umma_f16<CG>(d_tmem, adesc, bdesc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+#endif
             }
             if (leader) {
               if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, 0x3);

@@ -218,3 +218,31 @@ def test_stream_k_concurrent_streams_isolated(g):
             assert np.array_equal(gC.result().view(np.uint32), r.view(np.uint32))
             gC.full.copy_(torch.from_numpy(gC.full_host.copy()))
         torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+def test_stream_k_concurrent_across_window_wrap(g, acc):
+    # the token pool is cut into 32 fixed windows taken round robin; run enough
+    # concurrent stream-K GEMMs (4 streams x 12 rounds = 48 launches, plus the references)
+    # that the window index wraps while others are in flight -- every result must still be
+    # bitwise the one-at-a-time result (F32: fixed order of reduce-adds; F16: store, then add)
+    import torch
+    M, N, K = 1300, 2100, 2500
+    probs = [device_problem(M, N, K, acc, seed=50 + i) for i in range(4)]
+    ref = []
+    for A, B, C, gA, gB, gC in probs:
+        _run(g, gA, gB, gC, config="pair_256x256", max_clusters=5, stream_k=1)
+        ref.append(gC.result().copy())
+        gC.full.copy_(torch.from_numpy(gC.full_host.copy()))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in probs]
+    view = np.uint32 if acc == "f32" else np.uint16
+    for rep in range(12):
+        for s, (A, B, C, gA, gB, gC) in zip(streams, probs):
+            with torch.cuda.stream(s):
+                g.gemm_f16(gA.view, gB.view, gC.view, config="pair_256x256", max_clusters=5, stream_k=1)
+        torch.cuda.synchronize()
+        for r, (A, B, C, gA, gB, gC) in zip(ref, probs):
+            assert np.array_equal(gC.result().view(view), r.view(view)), rep
+            gC.full.copy_(torch.from_numpy(gC.full_host.copy()))
+        torch.cuda.synchronize()

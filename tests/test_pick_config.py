@@ -2,7 +2,8 @@
 "best performing version"), evaluated on the host for the B200's 148 SMs.
 
 Every expectation below is a measured winner (profiles/r01: cfgsweep.md, wide_tile.md,
-f32_short_k_cfg.txt, multicast.md, splitk.md v8/v9, mid_size_configs.txt).  The F32 chain
+f32_short_k_cfg.txt, multicast.md, splitk.md v8/v9, mid_size_configs.txt; profiles/r02:
+graph_small_pick*.jsonl for the split-K thresholds).  The F32 chain
 limit of the split-K configs (R4/R17) is checked as an invariant over a grid."""
 import itertools
 
@@ -35,22 +36,27 @@ CASES = [
     (32768, 1024, 4096, 1, "pair_256x256_k128"),
     (16384, 4096, 1024, 0, "pair_256x256"),          # F32 one K chunk, reduce-add epilogue
     (8192, 1002, 1000, 0, "pair_256x256_s5"),        # ... but a ragged N (N % 4 != 0) still stages C_in
-    (1024, 1024, 1024, 0, "splitk_128x128_s2"),      # F32: split in two even at K = 1024
+    (1024, 1024, 1024, 0, "solo_128x64"),            # r02: the two-way split loses below K = 4096
     (1024, 1024, 1024, 1, "solo_128x64"),
     (2048, 1024, 1024, 0, "solo_128x128"),           # at most half a wave of pair tiles
     (256, 1024, 16384, 1, "splitk_128x128_s4"),      # small output, long K
     (512, 512, 8192, 0, "splitk_128x128_s4"),
-    (1024, 1024, 4096, 0, "splitk_128x256_s4"),      # F32 prefers S4 from K = 4096
+    (1024, 1024, 4096, 0, "splitk_128x128_s2"),      # r02: F32 S2 x 128x128 at K = 4096 ...
+    (1024, 1024, 8192, 0, "splitk_128x256_s4"),      # ... S4 x 128x256 from K = 8192
     (1024, 1024, 4096, 1, "splitk_128x128_s2"),      # F16: the bulk-DMA S2 configs
     (1024, 1024, 8192, 1, "splitk_128x128_s2"),
     (1024, 1024, 16384, 1, "splitk_128x256_s4"),
-    (1024, 2048, 4096, 0, "splitk_128x256_s2"),
-    (1024, 1024, 2048, 0, "splitk_128x128_s2"),
-    (1024, 1024, 2048, 1, "splitk_128x128_s2"),
-    (1024, 512, 1024, 0, "splitk_128x128_s2"),
-    (768, 768, 2048, 0, "splitk_128x128_s2"),        # 36 x 4 CTAs would not fit in 4-CTA clusters
-    (768, 768, 2048, 1, "splitk_128x128_s2"),
-    (512, 512, 1024, 1, "solo_128x64"),              # F16 S2 only from K = 2048
+    (1024, 2048, 4096, 0, "solo_128x128"),           # r02: 17.7 vs 19.2 us for S2 x 128x256
+    (2048, 1024, 4096, 1, "solo_128x128"),           # r02: 17.9 vs 21.7 us
+    (1024, 1024, 2048, 0, "solo_128x64"),            # r02: 9.1 vs 10.0 us split
+    (1024, 1024, 2048, 1, "solo_128x64"),            # r02: 8.8 vs 10.8 us split
+    (1024, 512, 1024, 0, "solo_128x64"),
+    (768, 768, 2048, 0, "solo_128x64"),
+    (768, 768, 2048, 1, "solo_128x64"),
+    (768, 768, 4096, 0, "splitk_128x128_s2"),        # 36 x 4 CTAs would not fit in 4-CTA clusters
+    (768, 768, 4096, 1, "splitk_128x128_s2"),
+    (2048, 1024, 2048, 0, "solo_128x128"),           # r02: 11.7 vs 13.8 us for S2 x 128x256
+    (512, 512, 1024, 1, "solo_128x64"),              # S2 only from K = 4096
 ]
 
 

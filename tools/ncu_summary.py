@@ -20,6 +20,11 @@ KEYS = {
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum": "smem_bank_conflicts_st",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum": "smem_st_wavefronts",
     "smsp__sass_inst_executed_op_shared_st.sum": "smem_st_instructions",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
+    "lts__t_sectors.avg.pct_of_peak_sustained_elapsed": "l2_sector_throughput_pct",
+    "lts__t_bytes.sum": "l2_bytes",
+    "l1tex__m_xbar2l1tex_read_bytes.sum.pct_of_peak_sustained_elapsed": "l2_to_sm_pct_of_peak",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "compute_memory_throughput_pct",
 }
 
 
@@ -77,13 +82,14 @@ def main():
         res[name] = d
     with open(prefix + ".json", "w") as f:
         json.dump(res, f, indent=1)
-    lines = ["| capture | kernel | us | SM GHz | tensor % | DRAM rd GB | DRAM wr GB | L2->SM GB | L2 hit % | regs | smem wavefronts excessive |",
-             "|---|---|---|---|---|---|---|---|---|---|---|"]
+    lines = ["| capture | kernel | us | SM GHz | tensor % | DRAM rd GB | DRAM wr GB | L2->SM GB | L2 hit % | L2 throughput % of peak | DRAM throughput % | regs | smem wavefronts excessive |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for n, d in res.items():
         lines.append(f"| {n} | `{d['kernel'][:60]}` | {d.get('duration_us', 0):.1f} | {d.get('sm_clock_hz', 0)/1e9:.3f} | "
                      f"{d.get('tensor_pipe_active_pct', 0):.1f} | {d.get('dram_read_bytes', 0)/1e9:.3f} | "
                      f"{d.get('dram_write_bytes', 0)/1e9:.3f} | {d.get('l2_to_sm_bytes', 0)/1e9:.2f} | "
-                     f"{d.get('l2_hit_pct', 0):.1f} | {d.get('registers_per_thread', '')} | "
+                     f"{d.get('l2_hit_pct', 0):.1f} | {d.get('l2_throughput_pct', 'n/a')} | {d.get('dram_throughput_pct', 'n/a')} | "
+                     f"{d.get('registers_per_thread', '')} | "
                      f"{d.get('smem_wavefronts_excessive', 'n/a')} of {d.get('smem_wavefronts', 'n/a')} |")
     with open(prefix + ".md", "w") as f:
         f.write("\n".join(lines) + "\n")
