@@ -1,5 +1,5 @@
-"""A/B of option sets AND library builds in one process (round-robin blocks of back-to-back
-launches, medians): VARIANTS='[{"mode":"f32","config":"pair_256x512"},
+"""A/B of option sets AND library builds in one process (blocks of back-to-back launches in a
+shuffled order per round, medians): VARIANTS='[{"mode":"f32","config":"pair_256x512"},
 {"lib":"scratch/libA.so","mode":"f32","config":"pair_256x512","promote_k":-1}]'.
 A variant's "lib" swaps the binding's library handle (same ABI, another build)."""
 import ctypes, json, os, statistics, sys
@@ -27,8 +27,15 @@ for v in variants:
     for _ in range(3): run(v)
 torch.cuda.synchronize()
 res = {i: [] for i in range(len(variants))}
+import random
+rng = random.Random(0)
 for r in range(rounds):
-    for i, v in enumerate(variants):
+    # shuffled order per round: under the power cap the variant right after the round's
+    # Python gap runs on a cooler board (a fixed order favoured variant 0 by up to ~4 %)
+    order = list(range(len(variants)))
+    rng.shuffle(order)
+    for i in order:
+        v = variants[i]
         s, e = torch.cuda.Event(True), torch.cuda.Event(True)
         s.record()
         for _ in range(reps): run(v)
