@@ -35,12 +35,6 @@
 #pragma once
 #include "gemm_sm100.cuh"
 
-#ifndef G16_W32_SIMPLE
-#define G16_W32_SIMPLE 0    // A/B only: 1 = the plain loop of gemm_sm100_wide.cuh when no interior promotion
-#endif
-#ifndef G16_W32_TRYWAIT
-#define G16_W32_TRYWAIT 0   // A/B only: 1 = poll the accumulator barriers with the suspending try_wait
-#endif
 
 namespace g16 {
 
@@ -202,7 +196,6 @@ gemm_f16_sm100_wide_f32_kernel(const __grid_constant__ CUtensorMap tm_a,
       bool first[2] = {true, true};     // next MMA of the half starts a chain (accumulate = 0)
       int dlo[2] = {0, 0};              // first deferred k-block of a blocked / postponed half
       int dstage[2] = {0, 0};           // ... and its ring stage
-      bool return_mma = false;
       auto mma = [&](int st, int h) {
         const uint32_t a_s = sA + st * Cfg::A_BYTES;
         const uint32_t b_s = sB + st * Cfg::B_BYTES + h * Cfg::B_HALF_BYTES;
@@ -227,77 +220,15 @@ gemm_f16_sm100_wide_f32_kernel(const __grid_constant__ CUtensorMap tm_a,
       };
       // (test_wait: never suspends the issuer while the other half has work)
       auto try_unblock = [&](int h, int kend) {
-#if G16_W32_TRYWAIT
-        if (!blocked[h]) return;
-        const int done = __shfl_sync(0xffffffffu, mbar_try_wait(acce_bar + 8 * h, (ncommit[h] - 1u) & 1u) ? 1 : 0, 0);
-        if (!done) return;
-#else
         if (!blocked[h]) return;
         const int done = __shfl_sync(0xffffffffu, mbar_test_wait(acce_bar + 8 * h, (ncommit[h] - 1u) & 1u) ? 1 : 0, 0);
         if (!done) return;
-#endif
         tc_fence_after();
         blocked[h] = false;
         flush(h, kend);
       };
       int it = 0;
-#if G16_W32_SIMPLE
-      // A/B only: no interior promotion points -> the plain head / middle / tail loop of
-      // gemm_sm100_wide.cuh (isolates the cost of the generic deferral logic below)
-      if (p.kb_per_chunk >= KB) {
-        uint32_t acc_phase = 0;
-        for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
-          const bool tr = trace_me && leader && it < 60;
-          uint64_t clk0 = 0;
-          if (tr) { p.trace[8 * it + 0] = globaltimer_ns(); clk0 = clock64(); }
-          const int head = min(split, KB), tail = min(split, KB - head);
-          mbar_wait(acce_bar, acc_phase ^ 1u);
-          tc_fence_after();
-          {
-            int s = stage; uint32_t ph = phase;
-            for (int i = 0; i < head; ++i) {
-              mbar_wait(full_bar + 8 * s, ph); tc_fence_after();
-              first[0] = i == 0; mma(s, 0);
-              if (++s == RS) { s = 0; ph ^= 1u; }
-            }
-            if (tail == 0 && leader) umma_commit_pair(accf_bar, 0x3);
-            mbar_wait(acce_bar + 8, acc_phase ^ 1u);
-            tc_fence_after();
-            for (int i = 0; i < head; ++i) {
-              first[1] = i == 0; mma(stage, 1);
-              if (leader) umma_commit_pair(empty_bar + 8 * stage, 0x3);
-              if (++stage == RS) { stage = 0; phase ^= 1u; }
-            }
-            if (tail == 0 && leader) umma_commit_pair(accf_bar + 8, 0x3);
-          }
-          for (int kb = head; kb < KB - tail; ++kb) {
-            mbar_wait(full_bar + 8 * stage, phase); tc_fence_after();
-            mma(stage, 0); mma(stage, 1);
-            if (leader) umma_commit_pair(empty_bar + 8 * stage, 0x3);
-            if (++stage == RS) { stage = 0; phase ^= 1u; }
-          }
-          if (tail > 0) {
-            int s = stage; uint32_t ph = phase;
-            for (int i = 0; i < tail; ++i) {
-              mbar_wait(full_bar + 8 * s, ph); tc_fence_after();
-              mma(s, 0);
-              if (++s == RS) { s = 0; ph ^= 1u; }
-            }
-            if (leader) umma_commit_pair(accf_bar, 0x3);
-            for (int i = 0; i < tail; ++i) {
-              mma(stage, 1);
-              if (leader) umma_commit_pair(empty_bar + 8 * stage, 0x3);
-              if (++stage == RS) { stage = 0; phase ^= 1u; }
-            }
-            if (leader) umma_commit_pair(accf_bar + 8, 0x3);
-          }
-          if (tr) { p.trace[8 * it + 2] = globaltimer_ns(); p.trace[8 * it + 7] = clock64() - clk0; }
-          acc_phase ^= 1u;
-        }
-        return_mma = true;
-      }
-#endif
-      for (int tile = cluster; !return_mma && tile < p.num_tiles; tile += nclusters, ++it) {
+      for (int tile = cluster; tile < p.num_tiles; tile += nclusters, ++it) {
         const bool tr = trace_me && leader && it < 60;
         uint64_t clk0 = 0;
         if (tr) {
