@@ -428,6 +428,11 @@ int pick_config(int64_t M, int64_t N, int64_t K, int acc_type, int sm_count) {
   // 18.8 us F16; it loses ~4 % at K = 8192, where the deeper ring matters more;
   // profiles/r01/single_wave_cfg.txt)
   if (pair_tiles <= sm_count / 2 && K <= 4096) return GEMM_CFG_PAIR_256x256_S4;
+  // F32 C just over one wave (at most 1.25 waves) with 2048 < K <= 4096, where stream-K
+  // shares the extra tiles out: the S4 ring's 3 staging slots pipeline the extra partial
+  // store phases best (2304^3 31.0 -> 29.6 us, 2304 x 2560 x 2560 33.2 -> 31.4, 2304^2 x 4096
+  // 39.1 -> 37.9; not at K = 8192 or beyond 1.25 waves; profiles/r02/f32_one_wave_s4.jsonl)
+  if (acc_type == GEMM_ACC_F32 && K > 2048 && K <= 4096 && 4 * pair_tiles <= 5 * (sm_count / 2)) return GEMM_CFG_PAIR_256x256_S4;
   // F32 C with one K chunk: with the reduce-add epilogue (N % 4 == 0) C_in needs no
   // staging slot, and the 6-stage 64-deep ring is best (profiles/r01/f32_short_k_cfg.txt);
   // a ragged N still stages C_in and keeps the second slot of S5

@@ -26,6 +26,11 @@ CASES = [
     (2048, 2048, 4096, 1, "pair_256x256_s4"),
     (2048, 2048, 8192, 0, "pair_256x256_k128"),      # ... but not at K = 8192
     (2560, 2048, 2048, 0, "pair_256x256"),           # 80 pair tiles: more than one wave
+    (2304, 2304, 2304, 0, "pair_256x256_s4"),        # r02: F32 just over one wave, stream-K: S4
+    (2304, 2560, 2560, 0, "pair_256x256_s4"),
+    (2304, 2304, 4096, 0, "pair_256x256_s4"),
+    (2304, 2304, 8192, 0, "pair_256x256_k128"),      # ... not at K = 8192
+    (2560, 2560, 2560, 0, "pair_256x256_k128"),      # ... nor at 100 tiles (1.35 waves)
     (3072, 3072, 2048, 1, "pair_256x512"),
     (2304, 2304, 2304, 1, "pair_256x256_k128"),      # F16: stream-K over the partial last wave
     (2560, 2560, 8192, 1, "pair_256x256_k128"),
