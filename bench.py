@@ -373,16 +373,17 @@ def small_shapes(g, torch, synth, dev, peaks, reps=20, rounds=5):
         with torch.cuda.graph(graph, stream=s):
             for _ in range(reps):
                 g.gemm_f16(A, B, C, stream=s)
-        graph.replay()
-        torch.cuda.synchronize()
         ts = []
-        for _ in range(rounds):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(s)
+        with torch.cuda.stream(s):   # (replay() launches on the current stream: keep it = s)
             graph.replay()
-            e1.record(s)
             torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1) / reps * 1e3)
+            for _ in range(rounds):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                graph.replay()
+                e1.record(s)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) / reps * 1e3)
         us = statistics.median(ts)
         flops = 2.0 * n ** 3
         byts = 2 * (2 * n * n) + 2 * n * n * (4 if mode == "f32" else 2)
