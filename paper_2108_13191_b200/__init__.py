@@ -32,7 +32,7 @@ CONFIGS = {
     "pair_256x256_s5": 6,
     "pair_256x256_s4": 7,
     "pair_256x256_k128": 8,
-    "pair_256x512": 9,   # F16 C only
+    "pair_256x512": 9,   # AUTO picks it for F16 C; F32 C is selectable (measured slower)
     "splitk_128x256_s2": 10,
     "splitk_128x256_s4": 11,
     "splitk_128x128_s4": 12,

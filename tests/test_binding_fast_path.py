@@ -1,0 +1,69 @@
+"""The binding's fast path for the default call (`_gemm_f16_fast`, profiles/r02/findings.md §10):
+it must launch exactly what the general path launches (bitwise-equal C on the same inputs) and
+hand every unusual argument to the general path, so errors keep their precise types."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def g():
+    import torch
+    import paper_2108_13191_b200 as g
+    assert torch.cuda.is_available()
+    g.load_library()
+    return g
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+@pytest.mark.parametrize("shape", [(300, 520, 200), (1024, 1024, 1024), (8, 8, 8)])
+def test_fast_path_bitwise_equal_to_general_path(g, acc, shape):
+    import torch
+    M, N, K = shape
+    A, B, C = synth.problem(M, N, K, acc, seed=3)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    c_fast, c_gen = torch.from_numpy(C.copy()).cuda(), torch.from_numpy(C.copy()).cuda()
+    assert g._gemm_f16_fast(dA, dB, c_fast) is c_fast          # the fast path took it
+    g.gemm_f16(dA, dB, c_gen, config="auto")                     # the general path (its checks, _ld)
+    torch.cuda.synchronize()
+    bits = np.uint32 if acc == "f32" else np.uint16
+    assert np.array_equal(c_fast.cpu().numpy().view(bits), c_gen.cpu().numpy().view(bits))
+
+
+def test_fast_path_declines_unusual_arguments(g):
+    import torch
+    A = torch.zeros((64, 32), dtype=torch.float16, device="cuda")
+    B = torch.zeros((32, 48), dtype=torch.float16, device="cuda")
+    C = torch.zeros((64, 48), dtype=torch.float32, device="cuda")
+    cases = [
+        (A.cpu(), B, C),                                  # CPU operand
+        (A.bfloat16(), B.bfloat16(), C),                  # bf16 inputs (general path handles them)
+        (A, B, C.double()),                               # unsupported C type
+        (A, B[:16], C),                                   # K mismatch
+        (A.t().contiguous().t(), B, C),                   # column-major A
+        (A[:1], B, C[:1]),                                # a single row (leading-dim rule)
+        (A.reshape(-1), B, C),                            # not 2-D
+    ]
+    for a, b, c in cases:
+        assert g._gemm_f16_fast(a, b, c) is None
+
+
+def test_errors_keep_their_types_through_the_default_call(g):
+    import torch
+    A = torch.zeros((64, 32), dtype=torch.float16, device="cuda")
+    B = torch.zeros((32, 48), dtype=torch.float16, device="cuda")
+    C = torch.zeros((64, 48), dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        g.gemm_f16(A.cpu(), B, C)
+    with pytest.raises(TypeError):
+        g.gemm_f16(A, B, C.double())
+    with pytest.raises(ValueError):
+        g.gemm_f16(A, B[:16], C)
+    with pytest.raises(ValueError):
+        g.gemm_f16(A.t().contiguous().t(), B, C)
+    # a leading dimension the library rejects (stride 0 rows) comes back as a GemmError
+    with pytest.raises(g.GemmError):
+        g.gemm_f16(A[:1].expand(64, 32), B, C)
