@@ -17,6 +17,10 @@ CONFIGS = ["auto", "pair_256x256", "pair_256x128", "solo_128x256", "solo_128x128
            "pair_256x256_s5", "pair_256x256_s4", "pair_256x256_k128"]
 
 
+# the CTA-pair configurations built with stream-K (gemm_api.cu sk_fn_of: cta_group::2, no peers)
+STREAM_K_CONFIGS = {"pair_256x256", "pair_256x128", "pair_256x256_s5", "pair_256x256_s4", "pair_256x256_k128"}
+
+
 def _guarded_dev(host_bits, ld, rows_extra, canary):
     import torch
     full = np.full((host_bits.shape[0] + rows_extra, ld), canary, dtype=host_bits.dtype)
@@ -113,4 +117,8 @@ def _fuzz_case(case, seed, wide, configs=None):
     ex, _ = oracle.gemm(A, B, C, in_type=1 if bf16 else 0, beta=beta, bias=bias, relu=relu)
     Av = A.astype(np.float32) if not bf16 else torch.from_numpy(A.view(np.int16)).view(torch.bfloat16).float().numpy()
     Bv = B.astype(np.float32) if not bf16 else torch.from_numpy(B.view(np.int16)).view(torch.bfloat16).float().numpy()
-    check(got, ex, Av, Bv, acc, K, f"case {case}: {(M, N, K)} {acc} bf16={bf16} {kw} beta={beta} relu={relu} bias={use_bias}")
+    # a stream-K split tile with F16 C rounds twice more (DESIGN R18: rn16(C_in + p0), rn16(p1)),
+    # each time by up to half a binary16 ulp of a partial sum's magnitude (<= S)
+    sk_f16 = acc == "f16" and kw.get("stream_k") == 1 and kw["config"] in STREAM_K_CONFIGS
+    check(got, ex, Av, Bv, acc, K, f"case {case}: {(M, N, K)} {acc} bf16={bf16} {kw} beta={beta} relu={relu} bias={use_bias}",
+          C_in=C if beta else None, extra_roundings=2 if sk_f16 else 0)
