@@ -20,7 +20,7 @@ def g():
     return g
 
 
-def _sampled_check(g, M, N, K, acc, seed=0, n_random=24, **kw):
+def _sampled_check(g, M, N, K, acc, seed=0, n_random=24, extra_roundings=0, **kw):
     import torch
     A, B, C = synth.problem(M, N, K, acc, seed=seed)
     dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
@@ -32,7 +32,8 @@ def _sampled_check(g, M, N, K, acc, seed=0, n_random=24, **kw):
         rows = rows[keep]
     got = dC[torch.from_numpy(rows).cuda()].cpu().numpy()
     ex, _ = oracle.gemm(A, B, C, rows=rows)
-    return check(got, ex, A[rows], B, acc, K, f"{(M, N, K)} {acc} sampled")
+    return check(got, ex, A[rows], B, acc, K, f"{(M, N, K)} {acc} sampled", C_in=C[rows],
+                 extra_roundings=extra_roundings)
 
 
 @pytest.mark.parametrize("acc", ["f32", "f16"])
@@ -146,3 +147,43 @@ def test_symmetric_buffer_rendezvous_single_rank(g):
         check(t.cpu().numpy(), ex, A, B, "f32", K, "symmetric buffer")
     finally:
         dist.destroy_process_group()
+
+
+# round 2: the mid-size F32 rule (S4 ring with stream-K just over one wave) and the fused
+# epilogue options at multi-wave sizes (the fuzz covers them at <= 700 x 700)
+@pytest.mark.parametrize("shape", [(2304, 2304, 2304), (2304, 2560, 2560), (2304, 2304, 4096)])
+def test_one_wave_s4_stream_k_sampled(g, shape):
+    M, N, K = shape
+    for acc in ("f32", "f16"):
+        # F16 C takes stream-K here too (partial last wave, K > 2048): its split tiles round
+        # twice more (DESIGN R18), which the element gate allows for
+        _sampled_check(g, M, N, K, acc, n_random=8, extra_roundings=2 if acc == "f16" else 0)
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+@pytest.mark.parametrize("opt", ["bf16", "beta0", "bias_relu"])
+def test_epilogue_options_at_scale_sampled(g, acc, opt):
+    import torch
+    M = N = K = 4096
+    if opt == "bf16":
+        A, B, C = synth.problem_bf16(M, N, K, acc, seed=2)
+        tA = torch.from_numpy(A.view(np.int16)).cuda().view(torch.bfloat16)
+        tB = torch.from_numpy(B.view(np.int16)).cuda().view(torch.bfloat16)
+    else:
+        A, B, C = synth.problem(M, N, K, acc, seed=2)
+        tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    dC = torch.from_numpy(C.copy()).cuda()
+    bias = synth.uniform_f32(2, 3, 1, N)[0] if opt == "bias_relu" else None
+    kw = dict(beta=0 if opt == "beta0" else 1, relu=opt == "bias_relu",
+              bias=None if bias is None else torch.from_numpy(bias).cuda())
+    g.gemm_f16(tA, tB, dC, **kw)
+    torch.cuda.synchronize()
+    rows = synth.sample_rows(M, tile_m=128, n_random=8, seed=2)
+    got = dC[torch.from_numpy(rows).cuda()].cpu().numpy()
+    ex, _ = oracle.gemm(A, B, C, rows=rows, in_type=1 if opt == "bf16" else 0, beta=kw["beta"], bias=bias,
+                        relu=kw["relu"])
+    Av = (torch.from_numpy(A.view(np.int16)).view(torch.bfloat16).float().numpy() if opt == "bf16"
+          else A.astype(np.float32))
+    Bv = (torch.from_numpy(B.view(np.int16)).view(torch.bfloat16).float().numpy() if opt == "bf16"
+          else B.astype(np.float32))
+    check(got, ex, Av[rows], Bv, acc, K, f"4096^3 {acc} {opt} sampled", C_in=C[rows] if kw["beta"] else None)
