@@ -89,7 +89,12 @@ typedef enum {
                                      of the shared A box and TMA-multicasts it to the other three */
   GEMM_CFG_SOLO_128x128_MC4 = 14, /* as SOLO_128x128, with the same A multicast */
   GEMM_CFG_SPLITK_128x128_S2 = 15, /* as SPLITK_128x128_S4 with 2 CTAs (halves of K) per cluster */
-  GEMM_CFG_COUNT = 16
+  GEMM_CFG_PAIR2_256x256_MCB = 16, /* as PAIR_256x256_K128, two CTA pairs per 4-CTA cluster on
+                                      tiles (2t, n) and (2t+1, n): each pair loads half of the
+                                      shared B box and TMA-multicasts it into the other pair.  No
+                                      stream-K; selectable, not picked (4-CTA clusters fit on only
+                                      ~132 of 148 SMs) */
+  GEMM_CFG_COUNT = 17
 } gemm_config_t;
 
 typedef struct {

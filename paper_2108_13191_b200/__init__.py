@@ -39,6 +39,7 @@ CONFIGS = {
     "solo_128x64_mc4": 13,
     "solo_128x128_mc4": 14,
     "splitk_128x128_s2": 15,
+    "pair2_256x256_mcb": 16,   # B multicast across two CTA pairs (4-CTA clusters); not picked
 }
 _STATUS = {0: "GEMM_OK", 1: "GEMM_ERR_INVALID_VALUE", 2: "GEMM_ERR_MISALIGNED",
            3: "GEMM_ERR_UNSUPPORTED_DEVICE", 4: "GEMM_ERR_CUDA"}

@@ -76,6 +76,9 @@ using Cfg13F32 = KCfg<1, 64, 8, false, 1, 64, false, 4>;
 using Cfg13F16 = KCfg<1, 64, 8, true, 1, 64, false, 4>;
 using Cfg14F32 = KCfg<1, 128, 6, false, 1, 64, false, 4>;
 using Cfg14F16 = KCfg<1, 128, 6, true, 1, 64, false, 4>;
+// B multicast across the two CTA pairs of a 4-CTA cluster (the 128-deep pair config otherwise)
+using Cfg16F32 = KCfg<2, 256, 3, false, 1, 128, false, 2>;
+using Cfg16F16 = KCfg<2, 256, 3, true, 1, 128, false, 2>;
 // gemm_f16_gather: the 128-deep pair tile with peer stores compiled in
 using CfgGF32 = KCfg<2, 256, 3, false, 1, 128, true>;
 using CfgGF16 = KCfg<2, 256, 3, true, 1, 128, true>;
@@ -92,6 +95,7 @@ struct ConfigDesc {
   int cluster = 0;    // CTAs per cluster (0: = cta_group)
   int k_splits = 0;   // split-K configs: CTAs per cluster sharing one tile's K (non-persistent grid)
   int a_mc = 1;       // A-multicast configs: CTAs per cluster sharing A (tiles (tm, a_mc * tg + r))
+  int b_mc = 1;       // B-multicast configs: CTA pairs per cluster sharing B (tiles (b_mc * tg + p, tn))
   int cluster_size() const { return cluster ? cluster : cta_group; }
   KernelFn sk_fn[2] = {nullptr, nullptr};   // [acc_type]: the stream-K build (CTA-pair tiles only)
 };
@@ -107,7 +111,8 @@ constexpr ConfigDesc make_desc() {
   return ConfigDesc{C32::CG, C32::BN, C32::STAGES, C32::THREADS, C32::BK,
                     {C32::SMEM_BYTES, C16::SMEM_BYTES}, {C32::CW, C16::CW}, {C32::RB, C16::RB},
                     {&gemm_f16_sm100_kernel<C32>, &gemm_f16_sm100_kernel<C16>},
-                    C32::MC > 1 ? C32::MC : 0, 0, C32::MC,
+                    C32::MC > 1 ? C32::CG * C32::MC : 0, 0, C32::CG == 1 ? C32::MC : 1,
+                    C32::CG == 2 ? C32::MC : 1,
                     {sk_fn_of<C32>(), sk_fn_of<C16>()}};
 }
 
@@ -137,6 +142,7 @@ const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
     make_desc<Cfg13F32, Cfg13F16>(),
     make_desc<Cfg14F32, Cfg14F16>(),
     make_splitk_desc<128, 2>(),
+    make_desc<Cfg16F32, Cfg16F16>(),
 };
 using CfgW16 = WCfg<4>;
 // F32 C (gemm_sm100_wide_f32.cuh): ring depth and epilogue staging slots per warp
@@ -638,7 +644,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   p.K = static_cast<int>(K);
   const int tile_m = 128 * cd.cta_group;
   const int cl_size = cd.cluster_size();
-  p.tiles_m = static_cast<int>(cdiv(M, tile_m));
+  p.tiles_m = static_cast<int>(cdiv(cdiv(M, tile_m), cd.b_mc));     // (B multicast: groups of b_mc tiles)
   p.tiles_n = static_cast<int>(cdiv(cdiv(N, cd.tile_n), cd.a_mc));   // (A multicast: groups of a_mc tiles)
   const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n;
   if (tiles * std::max(1, cd.cluster_size()) > 0x7fffffffLL) return GEMM_ERR_INVALID_VALUE;

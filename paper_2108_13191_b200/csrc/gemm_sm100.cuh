@@ -177,8 +177,10 @@ struct KCfg {
   // epilogue staging in plain rows (32 lanes of a warp hit the same banks)
   static constexpr bool SW = SW_;
   static constexpr int CG = CG_;            // CTAs per MMA (cta_group)
-  static constexpr int MC = MC_;            // cta_group::1 only: CTAs per cluster sharing (multicasting) A
-  static_assert(MC == 1 || (CG == 1 && (MC == 2 || MC == 4)), "A multicast: 1-CTA tiles, 2 or 4 per cluster");
+  static constexpr int MC = MC_;            // cta_group::1: CTAs per cluster sharing (multicasting) A along N;
+                                            // cta_group::2: CTA pairs per cluster sharing B along M
+  static_assert(MC == 1 || (CG == 1 && (MC == 2 || MC == 4)) || (CG == 2 && MC == 2 && !PEERS_ && SW_),
+                "multicast: 1-CTA tiles 2 or 4 per cluster (A), or 2 CTA pairs per cluster (B)");
   static constexpr int BN = BN_;            // UMMA N (tile columns)
   static constexpr int STAGES = STAGES_;
   static constexpr bool OUT_F16 = OUT_F16_;
@@ -320,10 +322,15 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   const bool trace_me = p.trace != nullptr && blockIdx.x == static_cast<unsigned>(p.trace[8 * 63 + 7]);
   if (trace_me && threadIdx.x == 0) p.trace[8 * 62 + 0] = globaltimer_ns();
   constexpr int MC = Cfg::MC;
-  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
-  // A multicast (MC > 1): the MC CTAs of a cluster own tiles (tm, MC * tg + r), r = rank
-  // in the cluster; each loads 128 / MC rows of the shared A box and multicasts them
+  const uint32_t rank = (CG == 2) ? (cluster_ctarank() & 1u) : 0u;   // rank in the CTA pair
+  // A multicast (MC > 1, 1-CTA tiles): the MC CTAs of a cluster own tiles (tm, MC * tg + r),
+  // r = rank in the cluster; each loads 128 / MC rows of the shared A box and multicasts them.
+  // B multicast (MC = 2, CTA pairs): pair p of the cluster owns tile (2 * tg + p, tn); both pairs
+  // need the same B columns, so each loads one of the two 64-column atoms of a CTA's half and
+  // multicasts it into the same-rank CTA of the other pair
   const uint32_t mrank = (MC > 1) ? cluster_ctarank() : 0u;
+  const uint32_t pidx = (CG == 2 && MC > 1) ? (mrank >> 1) : 0u;   // pair within the cluster
+  const uint32_t lead = (CG == 2 && MC > 1) ? (mrank & ~1u) : 0u;  // cluster rank of this pair's leader
 
   if (warp == Cfg::W_PRODUCER && lane == 0) {
     prefetch_tmap(&tm_a);
@@ -367,7 +374,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     // waterfall around each TMA); the elected lane issues.
     {
       const bool leader = elect_one();
-      const uint32_t full_leader = (CG == 2) ? mapa_shared(full_bar, 0) : full_bar;
+      const uint32_t full_leader = (CG == 2) ? mapa_shared(full_bar, lead) : full_bar;
       const uint64_t pol_a = p.l2_hints ? policy_evict_last() : policy_evict_normal();
       const uint64_t pol_b = policy_evict_normal();
       int stage = 0;
@@ -378,7 +385,8 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
         const int tile = itm.tile;
         int tm, tn;
         tile_coords(tile, p, tm, tn);
-        if constexpr (MC > 1) tn = MC * tn + static_cast<int>(mrank);
+        if constexpr (MC > 1 && CG == 1) tn = MC * tn + static_cast<int>(mrank);
+        if constexpr (MC > 1 && CG == 2) tm = MC * tm + static_cast<int>(pidx);
         const int a_row = tm * BM * CG + static_cast<int>(rank) * BM;
         const int b_col = tn * BN + static_cast<int>(rank) * Cfg::BN_CTA;
         if (it + 1 == work.n_items && leader) griddep_launch_dependents();   // last tile: let the next grid ramp
@@ -401,6 +409,12 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
 #pragma unroll
               for (int g = 0; g < Cfg::BN_CTA / 8; ++g)
                 tma_load_2d_pair_hint(b_dst + kh * Cfg::B_HALF_BYTES + g * 1024, &tm_b, b_col + 8 * g, kc, fb, pol_b);
+            } else if constexpr (CG == 2 && MC > 1) {
+              tma_load_2d_pair_hint(a_dst + kh * Cfg::A_HALF_BYTES, &tm_a, kc, a_row, fb, pol_a);
+              static_assert(Cfg::BN_CTA / 64 == MC, "one B atom per pair");
+              tma_load_2d_pair_mc_hint(b_dst + kh * Cfg::B_HALF_BYTES + pidx * Cfg::B_ATOM_BYTES, &tm_b,
+                                       b_col + 64 * static_cast<int>(pidx), kc, fb,
+                                       static_cast<uint16_t>((1u << mrank) | (1u << (mrank ^ 2u))), pol_b);
             } else if constexpr (CG == 2) {
               tma_load_2d_pair_hint(a_dst + kh * Cfg::A_HALF_BYTES, &tm_a, kc, a_row, fb, pol_a);
 #pragma unroll
@@ -484,14 +498,15 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
 #endif
             }
             if (leader) {
-              if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, 0x3);
+              // (B multicast: a stage is refilled into both pairs, so both pairs' MMAs release it)
+              if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, MC > 1 ? 0xF : 0x3);
               else if constexpr (MC > 1) umma_commit_mc(empty_bar + 8 * stage, (1u << MC) - 1u);   // every CTA's stage
               else umma_commit(empty_bar + 8 * stage);
             }
             if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
           }
           if (leader) {
-            if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, 0x3);
+            if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, static_cast<uint16_t>(0x3u << (2u * pidx)));
             else umma_commit(accf_bar + 8 * acc);
           }
           if (tr && ch == n_chunks - 1) {
@@ -509,7 +524,7 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     const uint32_t hcol = (ew >> 2) * Cfg::CPW;   // first accumulator column of this warp
     const uint32_t ebuf0 = sE + ew * Cfg::EPI_SLOTS * Cfg::EPI_BUF;
     const uint32_t ebar0 = epi_bar + 8 * Cfg::EPI_SLOTS * ew;
-    const uint32_t acce_leader = (CG == 2) ? mapa_shared(acce_bar, 0) : acce_bar;
+    const uint32_t acce_leader = (CG == 2) ? mapa_shared(acce_bar, lead) : acce_bar;
     const uint64_t pol_c = p.l2_hints ? policy_evict_first() : policy_evict_normal();
     // F32 C, plain C += A.B: the staged accumulator is added into C by the TMA unit
     // (cp.reduce.async.bulk .add, one IEEE RN add in L2 -- bitwise the same C_in + acc),
@@ -531,7 +546,8 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
       const bool tr = trace_me && ew == 0 && lane == 0 && it < 60;
       int tm, tn;
       tile_coords(tile, p, tm, tn);
-      if constexpr (MC > 1) tn = MC * tn + static_cast<int>(mrank);
+      if constexpr (MC > 1 && CG == 1) tn = MC * tn + static_cast<int>(mrank);
+      if constexpr (MC > 1 && CG == 2) tm = MC * tm + static_cast<int>(pidx);
       const int row0 = tm * BM * CG + static_cast<int>(rank) * BM + static_cast<int>(q) * 32;
       const int col0 = tn * BN + static_cast<int>(hcol);
       // stream-K with F16 C: the second part of a split tile is added into C (which the first

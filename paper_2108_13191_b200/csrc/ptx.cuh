@@ -129,6 +129,17 @@ __device__ __forceinline__ void tma_load_2d_mc_hint(uint32_t dst, const CUtensor
       :: "r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar), "h"(mask), "l"(policy)
       : "memory");
 }
+// The CTA-pair load, multicast: the box lands at the same shared-memory offset in every CTA of
+// `mask`; each destination's bytes are counted on the barrier `bar` of that destination's pair
+// leader (`bar` is this CTA's pair-leader address, as for tma_load_2d_pair_hint).
+__device__ __forceinline__ void tma_load_2d_pair_mc_hint(uint32_t dst, const CUtensorMap* m, int32_t c0, int32_t c1,
+                                                         uint32_t bar, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;"
+      :: "r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar), "h"(mask), "l"(policy)
+      : "memory");
+}
 // 2-D tiled TMA store smem -> global (bulk_group completion).
 __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* m, int32_t c0, int32_t c1, uint32_t src,
                                                   uint64_t policy) {

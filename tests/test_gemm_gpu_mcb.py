@@ -1,0 +1,61 @@
+"""GEMM_CFG_PAIR2_256x256_MCB: two CTA pairs per 4-CTA cluster, the shared B box TMA-multicast
+between the pairs (north_star "clusters multicasting the shared operand").  Parity
+against the oracle on ragged shapes (odd pair-tile rows: the second pair of a cluster then runs
+wholly outside C), closed forms bit-exact, and determinism."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity import Guarded, check, device_problem, round_up
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def g():
+    import paper_2108_13191_b200 as g
+    g.load_library()
+    return g
+
+
+def _run(g, gA, gB, gC, **kw):
+    import torch
+    g.gemm_f16(gA.view, gB.view, gC.view, **kw)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+@pytest.mark.parametrize("shape", [(512, 256, 256), (768, 520, 300), (1300, 700, 1100), (256, 1024, 2048),
+                                   (2304, 1536, 640), (200, 130, 64)])
+def test_b_multicast_parity(g, acc, shape):
+    M, N, K = shape
+    A, B, C, gA, gB, gC = device_problem(M, N, K, acc, seed=7, pad=(8, 8, 8))
+    _run(g, gA, gB, gC, config="pair2_256x256_mcb")
+    ex, _ = oracle.gemm(A, B, C)
+    check(gC.result(), ex, A, B, acc, K, f"mcb {shape} {acc}", C_in=C)
+    assert gC.guard_intact()
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+def test_b_multicast_persistent_and_deterministic(g, acc):
+    # many tiles per cluster (phase wrap of the ring and the accumulators), bitwise equal to the
+    # 2-CTA pair kernel on small integers (exact) and run to run
+    import torch
+    M, N, K = 2048, 1024, 576
+    rng = np.random.default_rng(3)
+    A = rng.integers(-2, 3, (M, K)).astype(np.float16)
+    B = rng.integers(-2, 3, (K, N)).astype(np.float16)
+    C = rng.integers(-4, 5, (M, N)).astype(np.float32 if acc == "f32" else np.float16)
+    if acc == "f16":
+        A = np.clip(A, -1, 1).astype(np.float16); B = np.clip(B, -1, 1).astype(np.float16)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    outs = []
+    for cfg, mc in (("pair2_256x256_mcb", 1), ("pair2_256x256_mcb", 2), ("pair_256x256_k128", 1)):
+        dC = torch.from_numpy(C.copy()).cuda()
+        g.gemm_f16(dA, dB, dC, config=cfg, max_clusters=mc)
+        torch.cuda.synchronize()
+        outs.append(dC.cpu().numpy())
+    ex, rnd = oracle.gemm(A, B, C)
+    for o in outs:
+        assert np.array_equal(o, rnd)
