@@ -59,3 +59,31 @@ def test_b_multicast_persistent_and_deterministic(g, acc):
     ex, rnd = oracle.gemm(A, B, C)
     for o in outs:
         assert np.array_equal(o, rnd)
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+@pytest.mark.parametrize("opt", ["beta0", "bias_relu", "bf16", "promote_256", "acc_bufs_1"])
+def test_b_multicast_with_options(g, acc, opt):
+    import torch
+    M, N, K = 900, 520, 704
+    if opt == "bf16":
+        A, B, C = synth.problem_bf16(M, N, K, acc, seed=9)
+        tA = torch.from_numpy(A.view(np.int16)).cuda().view(torch.bfloat16)
+        tB = torch.from_numpy(B.view(np.int16)).cuda().view(torch.bfloat16)
+        Av = tA.float().cpu().numpy(); Bv = tB.float().cpu().numpy()
+    else:
+        A, B, C = synth.problem(M, N, K, acc, seed=9)
+        tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+        Av, Bv = A.astype(np.float32), B.astype(np.float32)
+    dC = torch.from_numpy(C.copy()).cuda()
+    bias = synth.uniform_f32(9, 3, 1, N)[0] if opt == "bias_relu" else None
+    kw = dict(config="pair2_256x256_mcb", beta=0 if opt == "beta0" else 1, relu=opt == "bias_relu",
+              bias=None if bias is None else torch.from_numpy(bias).cuda())
+    if opt == "promote_256":
+        kw["promote_k"] = 256
+    if opt == "acc_bufs_1":
+        kw["acc_bufs"] = 1
+    g.gemm_f16(tA, tB, dC, **kw)
+    torch.cuda.synchronize()
+    ex, _ = oracle.gemm(A, B, C, in_type=1 if opt == "bf16" else 0, beta=kw["beta"], bias=bias, relu=kw["relu"])
+    check(dC.cpu().numpy(), ex, Av, Bv, acc, K, f"mcb {opt} {acc}", C_in=C if kw["beta"] else None)
