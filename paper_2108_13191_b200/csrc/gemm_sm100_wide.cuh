@@ -307,6 +307,21 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
 #pragma unroll
         for (int i = 0; i < Cfg::CPW / 2; ++i) cv[i] = 0u;
       }
+      // ---- bias: this warp's 2 x 128 columns staged once per tile in its (now idle) staging
+      // slot, so the drain below reads them from shared memory (broadcast) instead of issuing
+      // a global load per element pair while the MMA may be waiting for the TMEM half
+      if constexpr (EXT) {
+        if (p.bias != nullptr) {
+          if (lane == 0 && !load_c) bulk_wait_group_read<0>();   // the previous tile's last store
+          __syncwarp();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float4 bb = load_bias4(p.bias, wide_col(tn, grp, h * Cfg::CPH + 4 * static_cast<int>(lane)), p.N);
+            sts128(ebuf + static_cast<uint32_t>(h * Cfg::CPH * 4) + 16u * lane, bb.x, bb.y, bb.z, bb.w);
+          }
+          __syncwarp();
+        }
+      }
       // ---- the accumulator, half by half: TMEM -> registers, + C_in (+ bias, relu),
       // one RNE rounding; each half goes back to the MMA warp as soon as it is read
 #pragma unroll
@@ -345,10 +360,10 @@ gemm_f16_sm100_wide_kernel(const __grid_constant__ CUtensorMap tm_a,
               const float2 ci = f16x2_to_f32(cvh[16 * c + j]);
               float o0 = ci.x + __uint_as_float(v[2 * j]);
               float o1 = ci.y + __uint_as_float(v[2 * j + 1]);
-              if (p.bias != nullptr) {
-                const int bc = wide_col(tn, grp, h * Cfg::CPH + 32 * c + 2 * j);
-                o0 += bc < p.N ? __ldg(p.bias + bc) : 0.f;
-                o1 += bc + 1 < p.N ? __ldg(p.bias + bc + 1) : 0.f;
+              if (p.bias != nullptr) {   // (staged above; columns past N hold 0)
+                const float2 bb = lds64f(ebuf + static_cast<uint32_t>(4 * (h * Cfg::CPH + 32 * c + 2 * j)));
+                o0 += bb.x;
+                o1 += bb.y;
               }
               if (p.relu) {
                 o0 = relu_keep_nan(o0);
