@@ -139,10 +139,10 @@ typedef struct {
                     /* grid before touching global memory); -1: off                        */
   int raster;       /* 0: default; 1: serpentine raster -- odd groups of group_m tile-rows */
                     /* walk their column strips right to left; -1: plain                   */
-  int c_reduce;     /* F32 C, plain C += A.B (no bias/ReLU, N % 4 == 0): 1 = the epilogue   */
-                    /* adds its tile into C with a TMA reduce-add store instead of loading */
-                    /* C_in into shared memory (bitwise the same single RN add); -1 = off; */
-                    /* 0 = default (on)                                                     */
+  int c_reduce;     /* F32 C, C += A.B (+ bias; no ReLU, N % 4 == 0): 1 = the epilogue adds */
+                    /* its tile into C with a TMA reduce-add store instead of loading C_in */
+                    /* into shared memory (without a bias bitwise the same single RN add;   */
+                    /* with one, C_in + RN(acc + bias)); -1 = off; 0 = default (on)         */
   int tail_ring;    /* 0: default (on); -1: off.  On a CTA's last tile, when no C_in is     */
                     /* staged, all output chunks are staged at once in the idle operand    */
                     /* ring and stored back to back (256x256-class pair, 1-CTA and        */

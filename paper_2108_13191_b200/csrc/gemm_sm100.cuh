@@ -526,12 +526,12 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
     const uint32_t ebar0 = epi_bar + 8 * Cfg::EPI_SLOTS * ew;
     const uint32_t acce_leader = (CG == 2) ? mapa_shared(acce_bar, lead) : acce_bar;
     const uint64_t pol_c = p.l2_hints ? policy_evict_first() : policy_evict_normal();
-    // F32 C, plain C += A.B: the staged accumulator is added into C by the TMA unit
-    // (cp.reduce.async.bulk .add, one IEEE RN add in L2 -- bitwise the same C_in + acc),
-    // so C_in is never loaded into shared memory: half the epilogue's shared-memory
-    // traffic and no C_in latency chain (findings.md section 14)
-    const bool red = !Cfg::OUT_F16 && !Cfg::PEERS && !p.beta0 && p.c_reduce && p.bias == nullptr && !p.relu &&
-                     !p.c_ragged;
+    // F32 C, C += A.B (+ bias): the staged accumulator (plus the bias, added in F32 first) is
+    // added into C by the TMA unit (cp.reduce.async.bulk .add, one IEEE RN add in L2 --
+    // bitwise the same C_in + acc when there is no bias), so C_in is never loaded into shared
+    // memory: half the epilogue's shared-memory traffic and no C_in latency chain (findings.md
+    // section 14).  ReLU needs the whole sum in registers, so it keeps the staged C_in path
+    const bool red = !Cfg::OUT_F16 && !Cfg::PEERS && !p.beta0 && p.c_reduce && !p.relu && !p.c_ragged;
     const bool load_c = !p.beta0 && !red;   // C_in traffic through the staging slots
     int acc = 0;
     uint32_t acc_phase = 0;

@@ -12,7 +12,9 @@ bias = torch.from_numpy(synth.uniform_f32(0, 3, 1, n)[0]).cuda()
 V = {"f32_f16in": lambda: g.gemm_f16(A, B, Cs["f32"]), "f32_bf16in": lambda: g.gemm_f16(Ab, Bb, Cs["f32"]),
      "f16_f16in": lambda: g.gemm_f16(A, B, Cs["f16"]), "f16_bf16in": lambda: g.gemm_f16(Ab, Bb, Cs["f16"]),
      "f32_beta0": lambda: g.gemm_f16(A, B, Cs["f32"], beta=0), "f32_bias_relu": lambda: g.gemm_f16(A, B, Cs["f32"], bias=bias, relu=True),
-     "f16_beta0": lambda: g.gemm_f16(A, B, Cs["f16"], beta=0), "f16_bias_relu": lambda: g.gemm_f16(A, B, Cs["f16"], bias=bias, relu=True)}
+     "f16_beta0": lambda: g.gemm_f16(A, B, Cs["f16"], beta=0), "f16_bias_relu": lambda: g.gemm_f16(A, B, Cs["f16"], bias=bias, relu=True),
+     "f32_bias": lambda: g.gemm_f16(A, B, Cs["f32"], bias=bias),
+     "f32_bias_staged": lambda: g.gemm_f16(A, B, Cs["f32"], bias=bias, c_reduce=-1)}
 for f in V.values(): f(); f()
 torch.cuda.synchronize()
 res = {k: [] for k in V}; rng = random.Random(0)
