@@ -183,6 +183,28 @@ def _check_operands(A, B, C, names=("A", "B", "C")):
 
 
 _fast_types = None   # (torch.float16, torch.float32, _cuda_getDevice, _cuda_getCurrentRawStream), set on first use
+_fastbind = None     # csrc/fastbind.cpp, when built (_build.build_fastbind); else the ctypes path below
+_fastbind_tried = False
+
+
+def _load_fastbind():
+    """Import the in-tree torch extension of the default call, if it was built, and hand it the
+    library's gemm_f16 entry point.  Absent or unloadable: None (the ctypes path is used)."""
+    global _fastbind, _fastbind_tried
+    _fastbind_tried = True
+    if _lib is None or not os.path.exists(_build.FASTBIND_SO):
+        return None
+    try:
+        import importlib.util
+        import torch  # noqa: F401  (the extension resolves libtorch symbols)
+        spec = importlib.util.spec_from_file_location("gemm_f16_fastbind", _build.FASTBIND_SO)
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        mod.set_entry(ctypes.cast(_lib.gemm_f16, ctypes.c_void_p).value)
+        _fastbind = mod
+    except Exception:   # a stale or foreign build: keep the ctypes path
+        _fastbind = None
+    return _fastbind
 
 
 def _gemm_f16_fast(A, B, C):
@@ -236,9 +258,17 @@ def gemm_f16(A, B, C, stream=None, config=0, beta: int = 1, bias=None, relu: boo
     receives per-tile timestamps (include/gemm_f16_diag.h).  Raises GemmError on a
     non-zero status.
     """
-    if (stream is None and not opts and config == 0 and beta == 1 and bias is None and not relu and not accum_f16
-            and trace is None and _gemm_f16_fast(A, B, C) is not None):
-        return C
+    if stream is None and not opts and config == 0 and beta == 1 and bias is None and not relu and not accum_f16 \
+            and trace is None:
+        fb = _fastbind if _fastbind_tried else (_load_fastbind() if _lib is not None else None)
+        if fb is not None:
+            st = fb.gemm_default(A, B, C)
+            if st == 0:
+                return C
+            if st > 0:
+                _check(st)
+        elif _gemm_f16_fast(A, B, C) is not None:
+            return C
     import torch
     lib = load_library()
     bad = set(opts) - set(_INT_OPTS)

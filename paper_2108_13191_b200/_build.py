@@ -37,6 +37,24 @@ def build_variant(out: str, defines=()) -> str:
     return out
 
 
+FASTBIND_DIR = os.path.join(PKG, "_fastbind")
+FASTBIND_SO = os.path.join(FASTBIND_DIR, "gemm_f16_fastbind.so")
+FASTBIND_SRC = os.path.join(CSRC, "fastbind.cpp")
+
+
+def build_fastbind(force: bool = False) -> str:
+    """The torch-tensor fast path of the Python binding (csrc/fastbind.cpp: argument marshalling
+    only), compiled in-tree with torch.utils.cpp_extension.  Optional: the ctypes path is used
+    when it is absent."""
+    if not force and os.path.exists(FASTBIND_SO) and os.path.getmtime(FASTBIND_SO) >= os.path.getmtime(FASTBIND_SRC):
+        return FASTBIND_SO
+    from torch.utils import cpp_extension
+    os.makedirs(FASTBIND_DIR, exist_ok=True)
+    cpp_extension.load(name="gemm_f16_fastbind", sources=[FASTBIND_SRC], build_directory=FASTBIND_DIR,
+                       extra_cflags=["-O2"], with_cuda=True, verbose=False)
+    return FASTBIND_SO
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB

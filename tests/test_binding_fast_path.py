@@ -67,3 +67,32 @@ def test_errors_keep_their_types_through_the_default_call(g):
     # a leading dimension the library rejects (stride 0 rows) comes back as a GemmError
     with pytest.raises(g.GemmError):
         g.gemm_f16(A[:1].expand(64, 32), B, C)
+
+
+def test_fastbind_extension_matches_the_general_path(g):
+    """The in-tree torch extension of the default call (csrc/fastbind.cpp), when built, is what
+    the default call uses; it launches exactly the general path's kernel and declines the rest."""
+    import os
+    import torch
+    from paper_2108_13191_b200 import _build
+    if not os.path.exists(_build.FASTBIND_SO):
+        pytest.skip("fastbind not built (the ctypes path is used)")
+    fb = g._load_fastbind()
+    assert fb is not None
+    for acc in ("f32", "f16"):
+        A, B, C = synth.problem(520, 384, 264, acc, seed=4)
+        dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+        c1, c2 = torch.from_numpy(C.copy()).cuda(), torch.from_numpy(C.copy()).cuda()
+        assert fb.gemm_default(dA, dB, c1) == 0
+        g.gemm_f16(dA, dB, c2, config="auto")
+        torch.cuda.synchronize()
+        bits = np.uint32 if acc == "f32" else np.uint16
+        assert np.array_equal(c1.cpu().numpy().view(bits), c2.cpu().numpy().view(bits))
+    A = torch.zeros((64, 32), dtype=torch.float16, device="cuda")
+    B = torch.zeros((32, 48), dtype=torch.float16, device="cuda")
+    C = torch.zeros((64, 48), dtype=torch.float32, device="cuda")
+    for a, b, c in [(A.cpu(), B, C), (A.bfloat16(), B.bfloat16(), C), (A, B, C.double()), (A, B[:16], C),
+                    (A.t().contiguous().t(), B, C), (A[:1], B, C[:1])]:
+        assert fb.gemm_default(a, b, c) == -1
+    # a leading dimension the library rejects comes back as its status (GEMM_ERR_INVALID_VALUE)
+    assert fb.gemm_default(A[:1].expand(64, 32), B, C) == 1
