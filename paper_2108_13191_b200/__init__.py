@@ -201,6 +201,7 @@ def _load_fastbind():
         mod = importlib.util.module_from_spec(spec)
         spec.loader.exec_module(mod)
         mod.set_entry(ctypes.cast(_lib.gemm_f16, ctypes.c_void_p).value)
+        mod.set_entry_ex(ctypes.cast(_lib.gemm_f16_ex, ctypes.c_void_p).value)
         _fastbind = mod
     except Exception:   # a stale or foreign build: keep the ctypes path
         _fastbind = None
@@ -258,16 +259,23 @@ def gemm_f16(A, B, C, stream=None, config=0, beta: int = 1, bias=None, relu: boo
     receives per-tile timestamps (include/gemm_f16_diag.h).  Raises GemmError on a
     non-zero status.
     """
-    if stream is None and not opts and config == 0 and beta == 1 and bias is None and not relu and not accum_f16 \
-            and trace is None:
+    if stream is None and not opts and not accum_f16 and trace is None and beta in (0, 1):
+        # the extension (csrc/fastbind.cpp) takes the default call and the common options (a
+        # configuration, beta = 0, ReLU, a bias); it declines (-1) anything else, which then
+        # takes the general path below and gets its precise error there
         fb = _fastbind if _fastbind_tried else (_load_fastbind() if _lib is not None else None)
+        plain = config == 0 and beta == 1 and bias is None and not relu
         if fb is not None:
-            st = fb.gemm_default(A, B, C)
+            if plain:
+                st = fb.gemm_default(A, B, C)
+            else:
+                cfg = CONFIGS[config] if isinstance(config, str) else int(config)
+                st = fb.gemm_options(A, B, C, cfg, 1 - int(beta), int(bool(relu)), bias)
             if st == 0:
                 return C
             if st > 0:
                 _check(st)
-        elif _gemm_f16_fast(A, B, C) is not None:
+        elif plain and _gemm_f16_fast(A, B, C) is not None:
             return C
     import torch
     lib = load_library()

@@ -91,8 +91,43 @@ def test_fastbind_extension_matches_the_general_path(g):
     A = torch.zeros((64, 32), dtype=torch.float16, device="cuda")
     B = torch.zeros((32, 48), dtype=torch.float16, device="cuda")
     C = torch.zeros((64, 48), dtype=torch.float32, device="cuda")
-    for a, b, c in [(A.cpu(), B, C), (A.bfloat16(), B.bfloat16(), C), (A, B, C.double()), (A, B[:16], C),
+    for a, b, c in [(A.cpu(), B, C), (A.bfloat16(), B, C), (A, B, C.double()), (A, B[:16], C),
                     (A.t().contiguous().t(), B, C), (A[:1], B, C[:1])]:
         assert fb.gemm_default(a, b, c) == -1
     # a leading dimension the library rejects comes back as its status (GEMM_ERR_INVALID_VALUE)
     assert fb.gemm_default(A[:1].expand(64, 32), B, C) == 1
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+def test_fastbind_options_match_the_general_path(g, acc):
+    """The extension's option entry (configuration, beta = 0, ReLU, bias, BF16 inputs) launches
+    the same kernels as the ctypes path of gemm_f16_ex: bitwise equal results."""
+    import os
+    import torch
+    from paper_2108_13191_b200 import _build
+    if not os.path.exists(_build.FASTBIND_SO):
+        pytest.skip("fastbind not built (the ctypes path is used)")
+    fb = g._load_fastbind()
+    M, N, K = 520, 384, 264
+    A, B, C = synth.problem(M, N, K, acc, seed=6)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    bias = torch.from_numpy(synth.uniform_f32(6, 3, 1, N)[0]).cuda()
+    cases = [dict(config=g.CONFIGS["solo_128x128"], beta0=0, relu=0, bias=None),
+             dict(config=0, beta0=1, relu=0, bias=None),
+             dict(config=0, beta0=0, relu=1, bias=bias),
+             dict(config=g.CONFIGS["pair_256x256"], beta0=0, relu=0, bias=bias)]
+    for bf16 in (False, True):
+        a, b = (dA.bfloat16(), dB.bfloat16()) if bf16 else (dA, dB)
+        for cs in cases:
+            c1, c2 = torch.from_numpy(C.copy()).cuda(), torch.from_numpy(C.copy()).cuda()
+            assert fb.gemm_options(a, b, c1, cs["config"], cs["beta0"], cs["relu"], cs["bias"]) == 0
+            # the ctypes path: gemm_f16_ex with the same options (a non-default knob value of 0 forces it)
+            g.gemm_f16(a, b, c2, config=cs["config"], beta=1 - cs["beta0"], relu=bool(cs["relu"]), bias=cs["bias"],
+                       stream=torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            bits = np.uint32 if acc == "f32" else np.uint16
+            assert np.array_equal(c1.cpu().numpy().view(bits), c2.cpu().numpy().view(bits)), (bf16, cs)
+    # a bias of the wrong length is declined (the Python path raises ValueError)
+    assert fb.gemm_options(dA, dB, torch.from_numpy(C.copy()).cuda(), 0, 0, 0, bias[:-1]) == -1
+    with pytest.raises(ValueError):
+        g.gemm_f16(dA, dB, torch.from_numpy(C.copy()).cuda(), bias=bias[:-1])
