@@ -94,7 +94,14 @@ typedef enum {
                                       shared B box and TMA-multicasts it into the other pair.  No
                                       stream-K; selectable, not picked (4-CTA clusters fit on only
                                       ~132 of 148 SMs) */
-  GEMM_CFG_COUNT = 17
+  GEMM_CFG_PAIR2_256x256_MCH = 17, /* the MCB kernel launched with cluster dim 2 and the preferred
+                                      cluster dim 4 (cudaLaunchAttributePreferredClusterDimension):
+                                      blocks 4i..4i+3 run as one 4-CTA cluster that multicasts B
+                                      where the hardware can place one (~132 of 148 SMs) and as two
+                                      2-CTA clusters that load B themselves elsewhere, so every SM
+                                      holds a CTA.  Same tiles, same order of operations: results
+                                      are bitwise those of PAIR_256x256_K128.  No stream-K */
+  GEMM_CFG_COUNT = 18
 } gemm_config_t;
 
 typedef struct {

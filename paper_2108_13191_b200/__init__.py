@@ -40,6 +40,7 @@ CONFIGS = {
     "solo_128x128_mc4": 14,
     "splitk_128x128_s2": 15,
     "pair2_256x256_mcb": 16,   # B multicast across two CTA pairs (4-CTA clusters); not picked
+    "pair2_256x256_mch": 17,   # the same kernel, preferred 4-CTA / regular 2-CTA clusters (all SMs)
 }
 _STATUS = {0: "GEMM_OK", 1: "GEMM_ERR_INVALID_VALUE", 2: "GEMM_ERR_MISALIGNED",
            3: "GEMM_ERR_UNSUPPORTED_DEVICE", 4: "GEMM_ERR_CUDA"}

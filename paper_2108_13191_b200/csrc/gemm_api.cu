@@ -96,8 +96,10 @@ struct ConfigDesc {
   int k_splits = 0;   // split-K configs: CTAs per cluster sharing one tile's K (non-persistent grid)
   int a_mc = 1;       // A-multicast configs: CTAs per cluster sharing A (tiles (tm, a_mc * tg + r))
   int b_mc = 1;       // B-multicast configs: CTA pairs per cluster sharing B (tiles (b_mc * tg + p, tn))
-  int cluster_size() const { return cluster ? cluster : cta_group; }
   KernelFn sk_fn[2] = {nullptr, nullptr};   // [acc_type]: the stream-K build (CTA-pair tiles only)
+  bool hybrid = false; // launched with cluster dim cta_group and the preferred cluster dim `cluster`
+  int cluster_size() const { return cluster ? cluster : cta_group; }
+  int launch_cluster() const { return hybrid ? cta_group : cluster_size(); }
 };
 
 template <class C>
@@ -143,6 +145,7 @@ const ConfigDesc kConfigs[GEMM_CFG_COUNT] = {
     make_desc<Cfg14F32, Cfg14F16>(),
     make_splitk_desc<128, 2>(),
     make_desc<Cfg16F32, Cfg16F16>(),
+    [] { ConfigDesc d = make_desc<Cfg16F32, Cfg16F16>(); d.hybrid = true; return d; }(),
 };
 using CfgW16 = WCfg<4>;
 // F32 C (gemm_sm100_wide_f32.cuh): ring depth and epilogue staging slots per warp
@@ -216,16 +219,20 @@ void init_device(int dev) {
         cudaLaunchConfig_t lc = {};
         cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = cs;
+        // (hybrid: occupancy of the regular 2-CTA clusters; a group of cs CTAs is one 4-CTA
+        // cluster or two 2-CTA ones, so all of them fit)
+        const int lcs = cd.launch_cluster();
+        attr[0].val.clusterDim.x = lcs;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
-        lc.gridDim = dim3(cs * (d.sm_count / cs), 1, 1);
+        lc.gridDim = dim3(lcs * (d.sm_count / lcs), 1, 1);
         lc.blockDim = dim3(cd.threads, 1, 1);
         lc.dynamicSmemBytes = cd.smem[a];
         lc.attrs = attr;
         lc.numAttrs = 1;
         int n = 0;
         e = cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(cd.fn[a]), &lc);
+        if (cd.hybrid) n = n * lcs / cs;
         if (e != cudaSuccess || n <= 0) { d.status = GEMM_ERR_CUDA; d.cuda_error = e ? e : cudaErrorInvalidConfiguration; return; }
         d.max_clusters[c][a] = n;
         if (cd.sk_fn[a] != nullptr) {   // the stream-K build: same smem, same cluster
@@ -701,17 +708,24 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (cd.k_splits) clusters = static_cast<int>(tiles);   // one tile per cluster (non-persistent)
 
   cudaLaunchConfig_t lc = {};
-  cudaLaunchAttribute attr[2];
   lc.gridDim = dim3(static_cast<unsigned>(clusters * cl_size), 1, 1);
   lc.blockDim = dim3(static_cast<unsigned>(cd.threads), 1, 1);
   lc.dynamicSmemBytes = cd.smem[a];
   lc.stream = stream;
+  cudaLaunchAttribute attr[3];
   if (cl_size > 1) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cl_size;
+    attr[0].val.clusterDim.x = cd.launch_cluster();
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     lc.numAttrs = 1;
+    if (cd.hybrid) {   // (the grid is a whole number of groups of cl_size CTAs)
+      attr[1].id = cudaLaunchAttributePreferredClusterDimension;
+      attr[1].val.preferredClusterDim.x = cl_size;
+      attr[1].val.preferredClusterDim.y = 1;
+      attr[1].val.preferredClusterDim.z = 1;
+      lc.numAttrs = 2;
+    }
   }
   const int raster = opts ? opts->raster : 0;
   if (raster < -1 || raster > 1) return GEMM_ERR_INVALID_VALUE;

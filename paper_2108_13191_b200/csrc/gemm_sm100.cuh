@@ -328,8 +328,14 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   // B multicast (MC = 2, CTA pairs): pair p of the cluster owns tile (2 * tg + p, tn); both pairs
   // need the same B columns, so each loads one of the two 64-column atoms of a CTA's half and
   // multicasts it into the same-rank CTA of the other pair
+  // Hybrid launch (GEMM_CFG_PAIR2_256x256_MCH: cluster dim 2, preferred cluster dim 4): the
+  // hardware groups blocks 4i..4i+3 into one 4-CTA cluster where it can place one (~132 of 148
+  // SMs) and into two 2-CTA clusters elsewhere.  The schedule is the same either way (pair
+  // (blockIdx / 2) % 2 of group blockIdx / 4 owns tile (2 tg + p, tn)); only a 4-CTA cluster
+  // multicasts B (`mc`), a lone pair loads both of its B atoms itself
   const uint32_t mrank = (MC > 1) ? cluster_ctarank() : 0u;
-  const uint32_t pidx = (CG == 2 && MC > 1) ? (mrank >> 1) : 0u;   // pair within the cluster
+  const bool mc = (CG == 2 && MC > 1) ? (cluster_nctarank() == 4u) : (MC > 1);
+  const uint32_t pidx = (CG == 2 && MC > 1) ? ((blockIdx.x >> 1) & 1u) : 0u;   // pair within the group of 4
   const uint32_t lead = (CG == 2 && MC > 1) ? (mrank & ~1u) : 0u;  // cluster rank of this pair's leader
 
   if (warp == Cfg::W_PRODUCER && lane == 0) {
@@ -342,7 +348,8 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   if (warp == Cfg::W_MMA && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar + 8 * s, 1);
-      mbar_init(empty_bar + 8 * s, MC);   // MC > 1: a stage is refilled once every CTA's MMAs used it
+      // MC > 1: a stage is refilled once every CTA's MMAs used it
+      mbar_init(empty_bar + 8 * s, (CG == 2 && MC > 1) ? (mc ? 2 : 1) : MC);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(accf_bar + 8 * b, 1);
@@ -412,9 +419,16 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
             } else if constexpr (CG == 2 && MC > 1) {
               tma_load_2d_pair_hint(a_dst + kh * Cfg::A_HALF_BYTES, &tm_a, kc, a_row, fb, pol_a);
               static_assert(Cfg::BN_CTA / 64 == MC, "one B atom per pair");
-              tma_load_2d_pair_mc_hint(b_dst + kh * Cfg::B_HALF_BYTES + pidx * Cfg::B_ATOM_BYTES, &tm_b,
-                                       b_col + 64 * static_cast<int>(pidx), kc, fb,
-                                       static_cast<uint16_t>((1u << mrank) | (1u << (mrank ^ 2u))), pol_b);
+              if (mc) {
+                tma_load_2d_pair_mc_hint(b_dst + kh * Cfg::B_HALF_BYTES + pidx * Cfg::B_ATOM_BYTES, &tm_b,
+                                         b_col + 64 * static_cast<int>(pidx), kc, fb,
+                                         static_cast<uint16_t>((1u << mrank) | (1u << (mrank ^ 2u))), pol_b);
+              } else {
+#pragma unroll
+                for (int h = 0; h < MC; ++h)
+                  tma_load_2d_pair_hint(b_dst + kh * Cfg::B_HALF_BYTES + h * Cfg::B_ATOM_BYTES, &tm_b, b_col + 64 * h,
+                                        kc, fb, pol_b);
+              }
             } else if constexpr (CG == 2) {
               tma_load_2d_pair_hint(a_dst + kh * Cfg::A_HALF_BYTES, &tm_a, kc, a_row, fb, pol_a);
 #pragma unroll
@@ -499,14 +513,14 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
             }
             if (leader) {
               // (B multicast: a stage is refilled into both pairs, so both pairs' MMAs release it)
-              if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, MC > 1 ? 0xF : 0x3);
+              if constexpr (CG == 2) umma_commit_pair(empty_bar + 8 * stage, mc ? 0xF : 0x3);
               else if constexpr (MC > 1) umma_commit_mc(empty_bar + 8 * stage, (1u << MC) - 1u);   // every CTA's stage
               else umma_commit(empty_bar + 8 * stage);
             }
             if (++stage == p.ring_stages) { stage = 0; phase ^= 1u; }
           }
           if (leader) {
-            if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, static_cast<uint16_t>(0x3u << (2u * pidx)));
+            if constexpr (CG == 2) umma_commit_pair(accf_bar + 8 * acc, static_cast<uint16_t>(0x3u << (mc ? 2u * pidx : 0u)));
             else umma_commit(accf_bar + 8 * acc);
           }
           if (tr && ch == n_chunks - 1) {
