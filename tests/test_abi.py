@@ -111,6 +111,19 @@ def test_config_info_is_host_only():
         g.config_info(99)
 
 
+def test_config_names_match_the_header_enum():
+    # the binding's config names are the header's gemm_config_t, value for value
+    import os
+    import re
+    hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "gemm_f16.h")).read()
+    enum = {m.group(1).lower(): int(m.group(2)) for m in re.finditer(r"GEMM_CFG_(\w+)\s*=\s*(\d+)", hdr)}
+    count = enum.pop("count")
+    assert enum.pop("auto") == 0 and g.CONFIGS.get("auto", 0) == 0
+    named = {k: v for k, v in g.CONFIGS.items() if k != "auto"}
+    assert named == enum
+    assert sorted(enum.values()) == list(range(1, count))
+
+
 def test_product_path_does_not_import_oracle():
     # the product package must never reach the oracle (no CPU fallback)
     pkg = os.path.join(ROOT, "paper_2108_13191_b200")

@@ -53,6 +53,13 @@ def test_fuzz_split_and_multicast_against_oracle(case):
     _fuzz_case(case, 30_000 + case, wide=False, configs=SPLIT_AND_MC)
 
 
+@pytest.mark.parametrize("case", range(N_EXTRA))
+def test_fuzz_b_multicast_against_oracle(case):
+    # the B-multicast kernel in 4-CTA clusters (mcb) and under the preferred-cluster launch (mch:
+    # 4-CTA clusters where they fit, lone pairs elsewhere)
+    _fuzz_case(case, 40_000 + case, wide=False, configs=["pair2_256x256_mcb", "pair2_256x256_mch"])
+
+
 def _fuzz_case(case, seed, wide, configs=None):
     import torch
     import paper_2108_13191_b200 as g
