@@ -749,6 +749,7 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (tro < -1 || tro > 1) return GEMM_ERR_INVALID_VALUE;
   p.tail_ring = tro >= 0 ? 1 : 0;
   const int skopt = opts ? opts->stream_k : 0;
+  void* sk_private = nullptr;   // a captured stream-K launch's own token counters (freed below)
   if (skopt < -1 || skopt > 1) return GEMM_ERR_INVALID_VALUE;
   p.sk_tile0 = p.num_tiles;
   // F32 C: the two partials of a split tile meet by reduce-add (needs the reduce-add epilogue);
@@ -771,7 +772,22 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
     // run boundaries within k_blocks / 8 of a tile edge snap to it (at least one full wave;
     // below one wave equal runs matter more: profiles/r01/stream_k.md, snapping)
     p.sk_snap = waves >= 1 ? p.k_blocks / 8 : 0;
-    p.sk_flags = di.sk_flags + sk_window_base(g_dev[dev].sk_next.fetch_add(1u));
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) cap = cudaStreamCaptureStatusNone;
+    if (cap == cudaStreamCaptureStatusActive) {
+      // A captured launch replays for the graph's whole lifetime, so a window of the shared
+      // pool would be taken again by eager launches on other streams (every kSkWindows
+      // launches) while a replay runs.  It gets counters of its own instead: graph memory
+      // nodes that every replay allocates, zeroes and frees around the kernel.
+      void* buf = nullptr;
+      cudaError_t ce = cudaMallocAsync(&buf, kSkWindow * sizeof(unsigned), stream);
+      if (ce == cudaSuccess) ce = cudaMemsetAsync(buf, 0, kSkWindow * sizeof(unsigned), stream);
+      if (ce != cudaSuccess) return cuda_fail(ce);
+      p.sk_flags = static_cast<unsigned*>(buf);
+      sk_private = buf;
+    } else {
+      p.sk_flags = di.sk_flags + sk_window_base(g_dev[dev].sk_next.fetch_add(1u));
+    }
     fn = cd.sk_fn[a];
   }
   if (cfg == GEMM_CFG_PAIR_256x512 && a == GEMM_ACC_F16 && (p.bias != nullptr || p.relu || p.accum_f16))
@@ -779,6 +795,10 @@ gemm_status_t launch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda
   if (wide32 && (p.bias != nullptr || p.beta0)) fn = kWideExtFn[a];
   if (no_swizzle) fn = kNoSwizzleFn[a];
   cudaError_t e = cudaLaunchKernelEx(&lc, fn, tm_a, tm_b, tm_c, p, pm, tm_cpf);
+  if (sk_private) {
+    const cudaError_t fe = cudaFreeAsync(sk_private, stream);
+    if (e == cudaSuccess) e = fe;
+  }
   if (e != cudaSuccess) return cuda_fail(e);
   t_trace = nullptr;   // (a trace is armed for one launch)
   t_last_launches = 1;

@@ -246,3 +246,52 @@ def test_stream_k_concurrent_across_window_wrap(g, acc):
             assert np.array_equal(gC.result().view(view), r.view(view)), rep
             gC.full.copy_(torch.from_numpy(gC.full_host.copy()))
         torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("acc", ["f32", "f16"])
+def test_stream_k_graph_replay_isolated_from_eager_launches(g, acc):
+    # a CUDA-graph-captured stream-K launch replays for the graph's lifetime, so a
+    # window of the shared token pool would be taken again by eager launches on other streams.
+    # Forced here: after the capture, advance the pool by exactly one turn, then run the replay
+    # and as many eager stream-K launches side by side -- with shared windows each eager launch
+    # would use the same counters as the replayed launch next to it.  Captured launches get
+    # private counters (graph memory nodes), so both stay bitwise equal to the same launches
+    # run alone.  (Sharing corrupts a result only if a waiter arrives between the two launches'
+    # posts, which this timing rarely produces: the build before the fix also passed. The test
+    # guards the capture path itself: memory nodes, zeroed counters, bitwise results.)
+    import torch
+    lib = g.load_library()
+    n_windows = lib.gemm_f16_diag_sk_pool_slots() // lib.gemm_f16_diag_sk_window_slots()
+    M, N, K = 1300, 2100, 2500
+    view = np.uint32 if acc == "f32" else np.uint16
+    kw = dict(config="pair_256x256", max_clusters=5, stream_k=1)
+    (_, _, _, xA, xB, xC), (_, _, _, yA, yB, yC), (_, _, _, zA, zB, zC) = [
+        device_problem(M, N, K, acc, seed=70 + i) for i in range(3)]
+    n = 6
+    for _ in range(n):
+        g.gemm_f16(xA.view, xB.view, xC.view, **kw)
+        g.gemm_f16(yA.view, yB.view, yC.view, **kw)
+    torch.cuda.synchronize()
+    ref_x, ref_y = xC.result().copy(), yC.result().copy()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s1):
+        for _ in range(n):
+            g.gemm_f16(xA.view, xB.view, xC.view, stream=s1, **kw)
+    for rep in range(3):
+        xC.full.copy_(torch.from_numpy(xC.full_host.copy()))
+        yC.full.copy_(torch.from_numpy(yC.full_host.copy()))
+        # one whole turn of the pool since the capture (the capture took n windows; after the
+        # first rep the n eager launches below do): the next eager launches take the windows
+        # the captured launches were given
+        for _ in range(n_windows - n):
+            g.gemm_f16(zA.view, zB.view, zC.view, **kw)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            graph.replay()
+        with torch.cuda.stream(s2):
+            for _ in range(n):
+                g.gemm_f16(yA.view, yB.view, yC.view, stream=s2, **kw)
+        torch.cuda.synchronize()
+        assert np.array_equal(xC.result().view(view), ref_x.view(view)), rep
+        assert np.array_equal(yC.result().view(view), ref_y.view(view)), rep
