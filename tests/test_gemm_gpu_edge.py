@@ -42,6 +42,10 @@ PATHS = [
     ("f16_splitk_s2", "f16", dict(config="splitk_128x128_s2")),
     ("f16_splitk_s4", "f16", dict(config="splitk_128x256_s4")),
     ("f16_streamk", "f16", dict(config="pair_256x256_k128", stream_k=1, max_clusters=4)),
+    ("f32_mch", "f32", dict(config="pair2_256x256_mch")),
+    ("f16_mch", "f16", dict(config="pair2_256x256_mch")),
+    ("f32_mcb", "f32", dict(config="pair2_256x256_mcb")),
+    ("f16_mcb", "f16", dict(config="pair2_256x256_mcb")),
 ]
 IDS = [p[0] for p in PATHS]
 M0, N0 = 700, 1300
