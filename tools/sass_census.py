@@ -10,6 +10,8 @@ SHIPPED = {   # file stem -> mangled-name fragment
     "sass_pair_256x256_k128_f32_reduce": "KCfgILi2ELi256ELi3ELb0ELi1ELi128ELb0ELi1ELb1EEELb0EE",
     "sass_pair_256x256_k128_f32_reduce_streamk": "KCfgILi2ELi256ELi3ELb0ELi1ELi128ELb0ELi1ELb1EEELb1EE",
     "sass_pair_256x512_f16_wide": "gemm_f16_sm100_wide_kernelINS_4WCfgILi4EEELb0EE",
+    # (selectable, not picked: the B-multicast kernel behind MCB and MCH)
+    "sass_pair2_256x256_mc_f32": "KCfgILi2ELi256ELi3ELb0ELi1ELi128ELb0ELi2ELb1EEELb0EE",
 }
 KEYS = ["UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "STTM", "UTMALDG", "UTMAREDG", "UTMASTG", "UTMAPF", "UBLKCP",
         "SYNCS", "ELECT", "STS", "LDS", "BAR", "HMMA"]
