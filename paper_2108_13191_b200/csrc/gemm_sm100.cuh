@@ -337,6 +337,10 @@ gemm_f16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
   const bool mc = (CG == 2 && MC > 1) ? (cluster_nctarank() == 4u) : (MC > 1);
   const uint32_t pidx = (CG == 2 && MC > 1) ? ((blockIdx.x >> 1) & 1u) : 0u;   // pair within the group of 4
   const uint32_t lead = (CG == 2 && MC > 1) ? (mrank & ~1u) : 0u;  // cluster rank of this pair's leader
+  // the schedule above assumes a cluster's CTAs are consecutive blocks (ctarank = blockIdx % size),
+  // which tools/probe_pref_cluster.cu measured for preferred clusters too; fail loudly otherwise
+  if constexpr (CG == 2 && MC > 1)
+    if (mrank != (blockIdx.x & (mc ? 3u : 1u))) __trap();
 
   if (warp == Cfg::W_PRODUCER && lane == 0) {
     prefetch_tmap(&tm_a);
